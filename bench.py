@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the α-DFT / α-FFT hot path (BASELINE.json metric:
+"α-FFT complex points/sec & % of HBM roofline at 1/2/4/8 B200 vs CPU oracle").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--method auto]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+    python bench.py --impl reference      # the reference CPU path (oracle port) on host cores
+
+Workload: BASELINE config 4 by default (65536 signals x N=8192 complex64,
+α = 1/8, M = N), the config the metric is quoted on at 1/2/4/8 GPUs; the
+batch is split into contiguous shards, one per rank, with no communication in
+the timed region (strong scaling of a fixed total batch).  A step is one
+transform of the rank's whole shard.  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="4", help="BASELINE config key: 0, 1a, 1b, 3, 4")
+    ap.add_argument("--method", default="auto", choices=["auto", "fft", "chirp", "direct"])
+    ap.add_argument("--impl", default="asx", choices=["asx", "reference"])
+    ap.add_argument("--batch", type=int, default=0, help="override total batch (testing)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work for the baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def shard_range(total: int, world: int, rank: int):
+    """Contiguous shard [lo, hi) of a batch of `total` signals."""
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def profiled_traffic(config_key: str, method: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(f"{config_key}:{method}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU reference
+
+def _cpu_worker(args):
+    key, lo, hi = args
+    import numpy as np
+
+    from oracle import alpha_oracle as orc  # CPU baseline leg only
+    from paper_2403_16665_b200.signals import WORKLOADS, generate
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    w = WORKLOADS[key]
+    x = generate(w, lo, hi - lo, threads=1).astype(np.complex128)
+    a, d = w.alpha.numerator, w.alpha.denominator
+    t0 = time.perf_counter()
+    for row in x:  # one signal per call, as the reference's transform_samples
+        if a == 1 and (w.n & (w.n - 1)) == 0:
+            orc.alpha_fft(row[None], a, d, w.m)
+        else:
+            orc.direct(row[None], a, d, w.m)
+    return time.perf_counter() - t0, hi - lo
+
+
+def cpu_reference(key: str, target_seconds: float):
+    """The reference's CPU path (oracle port of transform_samples / naive_forward)
+    on this host's cores, over a bounded seeded sample of the workload."""
+    import multiprocessing as mp
+
+    from paper_2403_16665_b200.signals import WORKLOADS
+
+    w = WORKLOADS[key]
+    cores = len(os.sched_getaffinity(0))
+    # calibrate one signal, then size the sample to ~target_seconds of CPU work
+    dt, _ = _cpu_worker((key, 0, 1))
+    per = max(dt, 1e-5)
+    sample = int(max(cores, min(w.batch, target_seconds / per)))
+    sample = max(cores, (sample // cores) * cores)
+    chunks = [(key, i * sample // cores, (i + 1) * sample // cores) for i in range(cores)]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, chunks)
+    wall = time.perf_counter() - t0
+    busy = max(r[0] for r in res)
+    value = sample * w.m / busy
+    return {"value": value, "unit": "complex points/s", "cores": cores, "kind": "port",
+            "sample": f"{sample} of {w.batch} signals of config {key} (per-signal oracle port of "
+                      f"ref transform_samples/naive_forward, {cores} processes, {busy:.2f} s busy, "
+                      f"{wall:.2f} s wall)"}
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_16665_b200 as asx
+    from paper_2403_16665_b200.signals import WORKLOADS, generate_device
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    w = WORKLOADS[args.config]
+    total = args.batch or w.batch
+    lo, hi = shard_range(total, world, rank)
+    nloc = hi - lo
+    x = generate_device(w, lo, nloc, device=dev)
+    plan = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, method=args.method, real_input=w.real,
+                    device=local)
+    out = torch.empty((nloc, w.m), dtype=getattr(torch, w.dtype), device=dev)
+    stream = torch.cuda.current_stream(dev)
+    bytes_step = w.bytes_alg(nloc)
+    flush = None
+    if bytes_step < 2 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        plan.execute(x, out=out)
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    with clocks:
+        for s, e in evs:
+            if flush is not None:
+                flush.zero_()
+            s.record(stream)
+            plan.execute(x, out=out)
+            e.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    tot_ms = sum(step_ms)
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms_max = float(t.item())
+    ms_per_step = tot_ms_max / args.steps
+    value = total * w.m / (ms_per_step / 1e3)
+    # roofline of the dominant (only) kernel: algorithmic bytes per launch / avg launch duration
+    avg_launch_s = (tot_ms / args.steps) / 1e3
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_step / avg_launch_s / 1e9
+    flops = w.flops_alg(nloc)
+
+    # e2e through the C ABI with host buffers (H2D + transform + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        hx.copy_(x)
+        hX = torch.empty((nloc, w.m), dtype=out.dtype, pin_memory=True)
+        hxn, hXn = hx.numpy(), hX.numpy()
+        plan.execute_host(hxn, out=hXn)  # warm-up (allocates the staging ring)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.execute_host(hxn, out=hXn)
+        el = time.perf_counter() - t0
+        barrier()
+        tt = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item()) / args.e2e_steps
+        elem_in = x.element_size()
+        e2e = {"value": total * w.m / e2e_s, "unit": "complex points/s",
+               "h2d_bytes_per_step": nloc * w.n * elem_in, "d2h_bytes_per_step": nloc * w.m * out.element_size(),
+               "ms_per_step": e2e_s * 1e3, "path": "asx_execute_host (C ABI, pinned host buffers)"}
+        # cross-check the host-path result against the device-path result (untimed)
+        same = torch.equal(hX.to(dev), out)
+        e2e["matches_device_path"] = bool(same)
+
+    # untimed verification collective: per-rank checksums gathered over NCCL
+    chk = torch.tensor([float(out.abs().amax().item()), float(out.real.sum().item())], dtype=torch.float64,
+                       device=dev)
+    if world > 1:
+        gathered = [torch.zeros_like(chk) for _ in range(world)]
+        dist.all_gather(gathered, chk)
+        checks = [g.tolist() for g in gathered]
+    else:
+        checks = [chk.tolist()]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(args.config, args.cpu_seconds)
+
+    if rank == 0:
+        dtype_arith = "f32" if w.dtype == "complex64" else "f64"
+        line = {
+            "metric": "alpha-FFT complex output points/sec",
+            "value": value,
+            "unit": "complex points/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": dtype_arith,
+            "data": "synthetic (BASELINE config tones+noise, numpy PCG64 per-signal seeds, tones synthesised on GPU)",
+            "config": {
+                "workload": f"config {w.key}: batch {total} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
+                "method": plan.method, "fft_size": plan.fft_size, "batch": total, "n": w.n, "m": w.m,
+                "alpha": str(w.alpha), "shard": f"contiguous {nloc} signals/rank",
+                "parallelism": f"dp{world} (batch shards, no data-path collective)",
+                "l2": "inputs larger than L2 (no flush)" if flush is None else "L2 flushed between steps",
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": profiled_traffic(args.config, plan.method),
+                "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)" if peak_kind == "measured"
+                else "fallback 6650 GB/s (B200_PROFILING.md)",
+                "bytes_alg_per_launch": bytes_step,
+                "flops_alg_per_launch": flops, "achieved_alg_tflops": flops / avg_launch_s / 1e12,
+                "kernel": {"fft": "k_afft", "chirp": "k_chirp", "direct": "k_direct"}[plan.method],
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * int(plan.info.kernels_per_execute),
+            "clocks": clocks.summary(),
+            "checksums": checks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on the host cores."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2403_16665_b200.signals import WORKLOADS
+
+    w = WORKLOADS[args.config]
+    vals = []
+    cpu = None
+    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
+        cpu = cpu_reference(args.config, args.cpu_seconds)
+        vals.append(cpu["value"])
+    value = statistics.median(vals)
+    cpu["value"] = value
+    line = {
+        "impl": "reference",
+        "metric": "alpha-FFT complex output points/sec",
+        "value": value,
+        "unit": "complex points/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": (w.batch * w.m / value) * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (same generator and config as the GPU arm)",
+        "config": {"workload": f"config {w.key}: batch {w.batch} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
+                   "batch": w.batch, "n": w.n, "m": w.m, "alpha": str(w.alpha)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": "complex points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

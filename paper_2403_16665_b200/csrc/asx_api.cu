@@ -1,0 +1,621 @@
+// asx_api.cu — C ABI of libasx.so (declared in include/asx.h).
+//
+// Host side of the drop-in boundary: plan validation mirrors the reference
+// (core.py:95-105 validate_pair, fastpath.py:85-110 plan), tables are built
+// on device at plan time, execute only launches kernels on the caller's
+// stream (no allocation, no host sync).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "../../include/asx.h"
+#include "asx_kernels.cuh"
+
+using namespace asx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(e == cudaErrorMemoryAllocation ? ASX_ERR_OOM : ASX_ERR_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                      \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+bool is_pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
+int log2i(int64_t v) {
+  int r = 0;
+  while ((int64_t(1) << r) < v) ++r;
+  return r;
+}
+int bit_length(int64_t v) {
+  int r = 0;
+  while (v) {
+    ++r;
+    v >>= 1;
+  }
+  return r;
+}
+
+constexpr int kMaxP_c64 = 16384;
+constexpr int kMaxP_c128 = 8192;
+
+}  // namespace
+
+struct asx_plan_s {
+  int64_t n = 0, m = 0, a = 1, d = 1;
+  int dtype = ASX_C128, real_input = 0, method = ASX_AUTO, device = 0;
+  int P = 0;
+  int64_t r = 1, fold = 1;
+  int64_t m_ref = 0;
+  int depth = -1, leaf = ASX_LEAF_NONE;
+  int64_t pred_mults = -1, pred_adds = -1;
+  // device tables
+  void* tables = nullptr;
+  size_t table_bytes = 0;
+  size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
+  int lfA = 0;
+  // execute_host resources
+  std::mutex host_mtx;
+  static constexpr int kLanes = 3;
+  cudaStream_t lane[kLanes] = {nullptr, nullptr, nullptr};
+  void* din[kLanes] = {nullptr, nullptr, nullptr};
+  void* dout[kLanes] = {nullptr, nullptr, nullptr};
+  int64_t lane_rows = 0;
+};
+
+namespace {
+
+size_t celem(int dtype) { return dtype == ASX_C64 ? sizeof(float2) : sizeof(double2); }
+size_t in_elem(const asx_plan_s* p) {
+  size_t re = p->dtype == ASX_C64 ? sizeof(float) : sizeof(double);
+  return p->real_input ? re : 2 * re;
+}
+
+// --------------------------- kernel dispatch --------------------------------
+
+template <int P, typename Real> struct Cfg {
+  static constexpr int R = (P <= 32) ? P : ((P >= 16384) ? 32 : 16);
+  static constexpr int NT = P / R;
+  static constexpr int TPB = (NT >= 256) ? 1 : (NT == 1 ? 64 : 256 / NT);
+  using E = Fft<Real, P, NT>;
+  static constexpr size_t SMEM = size_t(TPB) * E::SMEM_ELEMS * sizeof(typename CT<Real>::T);
+};
+
+template <typename KernelT>
+cudaError_t prep_smem(KernelT kern, size_t smem) {
+  if (smem > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaSuccess;
+}
+
+template <typename Real, int P>
+cudaError_t launch_fft_family(int which, const KParams& kp, int64_t units, cudaStream_t st) {
+  using G = Cfg<P, Real>;
+  const int64_t blocks = (units + G::TPB - 1) / G::TPB;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  if (which == ASX_FFT) {
+    auto kern = k_afft<Real, P, G::NT, G::TPB>;
+    cudaError_t e = prep_smem(kern, G::SMEM);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)blocks, G::NT * G::TPB, G::SMEM, st>>>(kp);
+  } else {
+    auto kern = k_chirp<Real, P, G::NT, G::TPB>;
+    cudaError_t e = prep_smem(kern, G::SMEM);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)blocks, G::NT * G::TPB, G::SMEM, st>>>(kp);
+  }
+  return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t units, cudaStream_t st) {
+  switch (P) {
+#define ASX_CASE(S) \
+  case S:           \
+    return launch_fft_family<Real, S>(which, kp, units, st);
+    ASX_CASE(1)
+    ASX_CASE(2)
+    ASX_CASE(4)
+    ASX_CASE(8)
+    ASX_CASE(16)
+    ASX_CASE(32)
+    ASX_CASE(64)
+    ASX_CASE(128)
+    ASX_CASE(256)
+    ASX_CASE(512)
+    ASX_CASE(1024)
+    ASX_CASE(2048)
+    ASX_CASE(4096)
+    ASX_CASE(8192)
+#undef ASX_CASE
+    case 16384:
+      if constexpr (sizeof(Real) == 4) return launch_fft_family<Real, 16384>(which, kp, units, st);
+      return cudaErrorInvalidValue;
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+int two_level_lf(int64_t L) { return (log2i(L) + 1) / 2; }
+
+// Builds [fine(F) | coarse(ceil(L/F))] for W_L at dst.
+void fill_two_level(void* dst, int64_t L, int lf, int dbl, cudaStream_t st) {
+  const int64_t F = int64_t(1) << lf;
+  const int64_t coarse = (L + F - 1) / F;
+  const size_t es = dbl ? sizeof(double2) : sizeof(float2);
+  k_fill_roots<<<(unsigned)std::min<int64_t>((F + 255) / 256, 4096), 256, 0, st>>>(dst, F, 1, (uint64_t)L, dbl);
+  k_fill_roots<<<(unsigned)std::min<int64_t>((coarse + 255) / 256, 4096), 256, 0, st>>>(
+      static_cast<char*>(dst) + F * es, coarse, (uint64_t)F, (uint64_t)L, dbl);
+}
+int64_t two_level_size(int64_t L, int lf) {
+  const int64_t F = int64_t(1) << lf;
+  return F + (L + F - 1) / F;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    ok = (cudaSetDevice(dev) == cudaSuccess);
+    if (!ok) cudaGetLastError();
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int64_t next_pow2(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+void fill_kparams(const asx_plan_s* p, KParams& kp) {
+  std::memset(&kp, 0, sizeof(kp));
+  kp.n = p->n;
+  kp.m = p->m;
+  kp.r = p->r;
+  kp.fold = p->fold;
+  kp.real_in = p->real_input;
+  kp.lfA = p->lfA;
+  char* base = static_cast<char*>(p->tables);
+  kp.twP = base + p->off_twP;
+  kp.twA = base + p->off_twA;
+  kp.chirp = base + p->off_chirp;
+  kp.H = base + p->off_H;
+  kp.W = base + p->off_W;
+}
+
+int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs, int64_t batch,
+                   cudaStream_t st) {
+  if (batch == 0 || p->m == 0) return ASX_OK;
+  KParams kp;
+  fill_kparams(p, kp);
+  kp.x = x;
+  kp.xs = xs;
+  kp.X = X;
+  kp.Xs = Xs;
+  kp.batch = batch;
+  cudaError_t e = cudaSuccess;
+  if (p->method == ASX_DIRECT) {
+    const int64_t gy = (batch + 63) / 64, gx = (p->m + 63) / 64;
+    if (gy > 65535) {
+      // grid.y limit: walk the batch in slabs of 65535*64 signals
+      const int64_t slab = 65535LL * 64;
+      for (int64_t b0 = 0; b0 < batch; b0 += slab) {
+        KParams k2 = kp;
+        k2.x = static_cast<const char*>(x) + b0 * xs * in_elem(p);
+        k2.X = static_cast<char*>(X) + b0 * Xs * celem(p->dtype);
+        k2.batch = std::min(slab, batch - b0);
+        dim3 grid((unsigned)gx, (unsigned)((k2.batch + 63) / 64));
+        if (p->dtype == ASX_C64)
+          k_direct<float><<<grid, 256, 0, st>>>(k2);
+        else
+          k_direct<double><<<grid, 256, 0, st>>>(k2);
+      }
+    } else {
+      dim3 grid((unsigned)gx, (unsigned)gy);
+      if (p->dtype == ASX_C64)
+        k_direct<float><<<grid, 256, 0, st>>>(kp);
+      else
+        k_direct<double><<<grid, 256, 0, st>>>(kp);
+    }
+    e = cudaGetLastError();
+  } else {
+    const int64_t units = (p->method == ASX_FFT) ? batch * p->r : batch;
+    if (p->dtype == ASX_C64)
+      e = launch_by_size<float>(p->method, p->P, kp, units, st);
+    else
+      e = launch_by_size<double>(p->method, p->P, kp, units, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "asx_execute launch");
+  return ASX_OK;
+}
+
+}  // namespace
+
+// ================================ C ABI =====================================
+
+extern "C" {
+
+int asx_version(void) { return ASX_ABI_VERSION; }
+
+const char* asx_strerror(int status) {
+  switch (status) {
+    case ASX_OK: return "ok";
+    case ASX_ERR_INVALID: return "invalid argument";
+    case ASX_ERR_INCOMPATIBLE: return "density factor incompatible with signal length (alpha*N not an integer)";
+    case ASX_ERR_UNSUPPORTED: return "unsupported size for this method";
+    case ASX_ERR_CUDA: return "CUDA error";
+    case ASX_ERR_OOM: return "device out of memory";
+    default: return "unknown status";
+  }
+}
+
+const char* asx_last_error(void) { return g_last_error.c_str(); }
+
+int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, int64_t m, int dtype,
+                    int real_input, int method, int device) {
+  if (!out) return fail(ASX_ERR_INVALID, "plan pointer is NULL");
+  *out = nullptr;
+  if (n < 1) return fail(ASX_ERR_INVALID, "signal length must be >= 1, got " + std::to_string(n));
+  if (a_num < 1 || a_den < 1)
+    return fail(ASX_ERR_INVALID, "density factor must be positive, got " + std::to_string(a_num) + "/" +
+                                     std::to_string(a_den));
+  if (dtype != ASX_C64 && dtype != ASX_C128) return fail(ASX_ERR_INVALID, "dtype must be ASX_C64 or ASX_C128");
+  if (method < ASX_AUTO || method > ASX_CHIRP) return fail(ASX_ERR_INVALID, "unknown method");
+  const int64_t g = gcd64(a_num, a_den);
+  const int64_t a = a_num / g, d = a_den / g;  // α = a/d ; reference α_ref = d/a
+  // Reference full-spectrum size (core.py:95-105 with DenseFactor(d, a)).
+  const bool integral = ((n * d) % a) == 0;
+  const int64_t m_ref = integral ? (n * d) / a : 0;
+  if (m <= 0) {
+    if (!integral)
+      return fail(ASX_ERR_INCOMPATIBLE, "density factor " + std::to_string(d) + "/" + std::to_string(a) +
+                                            " is incompatible with N=" + std::to_string(n) + ": alpha*N = " +
+                                            std::to_string(n * d) + "/" + std::to_string(a) +
+                                            " is not an integer");
+    m = m_ref;
+  }
+  if (d > (int64_t(1) << 20) || a > (int64_t(1) << 20) || n > (int64_t(1) << 26))
+    return fail(ASX_ERR_UNSUPPORTED, "alpha terms or N beyond the exact-reduction range");
+
+  const int maxP = dtype == ASX_C64 ? kMaxP_c64 : kMaxP_c128;
+  // α-FFT applicability (reference plan(): power-of-two N and alpha*N,
+  // fastpath.py:97-101; generalised to any integer density r = d (a == 1),
+  // or integer decimation fold = a with N/a a power of two (d == 1)).
+  bool fft_ok = false;
+  int64_t fft_r = 1, fft_fold = 1, fft_P = 0;
+  if (a == 1 && is_pow2(n) && n <= maxP) {
+    fft_ok = true;
+    fft_r = d;
+    fft_P = n;
+  } else if (d == 1 && n % a == 0 && is_pow2(n / a) && (n / a) <= maxP) {
+    fft_ok = true;
+    fft_fold = a;
+    fft_P = n / a;
+  }
+  const int64_t chirp_P = next_pow2(n + m - 1);
+  const bool chirp_ok = chirp_P <= maxP;
+
+  auto lg = [](int64_t v) { return (double)std::max(1, log2i(v)); };
+  const double cost_direct = 8.0 * (double)n * (double)m * 0.5;
+  const double cost_fft = fft_ok ? (double)fft_r * (5.0 * fft_P * lg(fft_P) + 8.0 * fft_P) +
+                                       (double)fft_fold * fft_P * 2.0
+                                 : 1e300;
+  const double cost_chirp = chirp_ok ? 2.0 * 5.0 * chirp_P * lg(chirp_P) + 24.0 * chirp_P : 1e300;
+
+  int chosen = method;
+  if (method == ASX_AUTO) {
+    chosen = ASX_DIRECT;
+    double best = cost_direct;
+    if (cost_fft < best) {
+      best = cost_fft;
+      chosen = ASX_FFT;
+    }
+    if (cost_chirp < best) {
+      best = cost_chirp;
+      chosen = ASX_CHIRP;
+    }
+  } else if (method == ASX_FFT && !fft_ok) {
+    return fail(ASX_ERR_UNSUPPORTED,
+                "fast path needs power-of-two N and an integer density (alpha = 1/r) or a power-of-two "
+                "decimation (alpha = q, N/q a power of two), N <= " +
+                    std::to_string(maxP) + "; got N=" + std::to_string(n) + ", alpha=" + std::to_string(a) + "/" +
+                    std::to_string(d) + "; use the naive transform for this pair");
+  } else if (method == ASX_CHIRP && !chirp_ok) {
+    return fail(ASX_ERR_UNSUPPORTED, "chirp path needs N+M-1 <= " + std::to_string(maxP) + " for this dtype");
+  }
+  if (chosen == ASX_DIRECT && (n * m > (int64_t(1) << 31)))
+    return fail(ASX_ERR_UNSUPPORTED, "direct W matrix beyond 2^31 entries; use method fft/chirp");
+
+  asx_plan_s* p = new (std::nothrow) asx_plan_s();
+  if (!p) return fail(ASX_ERR_OOM, "host allocation failed");
+  p->n = n;
+  p->m = m;
+  p->a = a;
+  p->d = d;
+  p->dtype = dtype;
+  p->real_input = real_input ? 1 : 0;
+  p->method = chosen;
+  p->device = device;
+  p->m_ref = m_ref;
+  if (integral) {
+    p->depth = bit_length(std::min(n, m_ref)) - 1;  // fastpath.py:102
+    p->leaf = (d >= a) ? ASX_LEAF_SINGLE_SAMPLE : ASX_LEAF_BLOCK_SUM;  // fastpath.py:103
+    p->pred_mults = (m_ref / 2) * p->depth;                              // fastpath.py:113-121
+    p->pred_adds = m_ref * p->depth + (m_ref < n ? n - m_ref : 0);       // fastpath.py:124-127
+  }
+
+  DeviceGuard guard(device);
+  if (!guard.ok) {
+    delete p;
+    return fail(ASX_ERR_CUDA, "cannot select CUDA device " + std::to_string(device) + " (no GPU?)");
+  }
+  const int dbl = dtype == ASX_C128;
+  const size_t es = celem(dtype);
+  // ---- table layout ----
+  size_t elems = 0;
+  int64_t twP_sz = 0, twA_sz = 0, chirp_sz = 0, H_sz = 0, W_sz = 0;
+  if (chosen == ASX_FFT) {
+    p->P = (int)fft_P;
+    p->r = fft_r;
+    p->fold = fft_fold;
+  }
+  // must equal TwSplit<P>::LF (asx_engine.cuh)
+  auto lf_of_P = [](int P) {
+    const int LP = log2i(P);
+    return (LP + 1) / 2;
+  };
+  if (chosen == ASX_FFT || chosen == ASX_CHIRP) {
+    if (chosen == ASX_CHIRP) p->P = (int)chirp_P;
+    twP_sz = two_level_size(p->P, lf_of_P(p->P));
+  }
+  if (chosen == ASX_FFT && p->r > 1) {
+    p->lfA = two_level_lf(p->r * p->P);
+    twA_sz = two_level_size(p->r * p->P, p->lfA);
+  }
+  if (chosen == ASX_CHIRP) {
+    chirp_sz = std::max(n, m);
+    H_sz = p->P;
+  }
+  if (chosen == ASX_DIRECT) W_sz = m * n;
+  auto align = [](size_t v) { return (v + 31) & ~size_t(31); };
+  p->off_twP = 0;
+  elems = align(twP_sz);
+  p->off_twA = elems * es;
+  elems += align(twA_sz);
+  p->off_chirp = elems * es;
+  elems += align(chirp_sz);
+  p->off_H = elems * es;
+  elems += align(H_sz);
+  p->off_W = elems * es;
+  elems += align(W_sz);
+  p->table_bytes = std::max<size_t>(elems * es, 64);
+
+  cudaError_t e = cudaMalloc(&p->tables, p->table_bytes);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "cudaMalloc(plan tables)");
+  }
+  cudaStream_t st = nullptr;
+  e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    cudaFree(p->tables);
+    delete p;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  char* base = static_cast<char*>(p->tables);
+  if (twP_sz) fill_two_level(base + p->off_twP, p->P, lf_of_P(p->P), dbl, st);
+  if (twA_sz) fill_two_level(base + p->off_twA, p->r * p->P, p->lfA, dbl, st);
+  double2* wP_d = nullptr;
+  if (chosen == ASX_CHIRP) {
+    const uint64_t L2 = 2ull * (uint64_t)d * (uint64_t)n;
+    k_fill_chirp<<<(unsigned)std::min<int64_t>((chirp_sz + 255) / 256, 4096), 256, 0, st>>>(
+        base + p->off_chirp, chirp_sz, (uint64_t)a, L2, dbl);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), sizeof(double2) * p->P, st);
+    if (e == cudaSuccess) {
+      k_fill_roots<<<(p->P + 255) / 256, 256, 0, st>>>(wP_d, p->P, 1, (uint64_t)p->P, 1);
+      k_chirp_spectrum<<<(p->P + 127) / 128, 128, 0, st>>>(base + p->off_H, p->P, n, m, (uint64_t)a, L2, wP_d,
+                                                           dbl);
+      cudaFreeAsync(wP_d, st);
+    }
+  }
+  if (chosen == ASX_DIRECT) {
+    const uint64_t L = (uint64_t)d * (uint64_t)n;
+    const int64_t total = m * n;
+    k_dft_matrix<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
+        base + p->off_W, m, n, (uint64_t)a, L, dbl);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess) {
+    cudaFree(p->tables);
+    delete p;
+    return cuda_fail(e, "plan table build");
+  }
+  *out = p;
+  return ASX_OK;
+}
+
+int asx_plan_destroy(asx_plan_t p) {
+  if (!p) return ASX_OK;
+  {
+    DeviceGuard guard(p->device);
+    for (int i = 0; i < asx_plan_s::kLanes; ++i) {
+      if (p->lane[i]) cudaStreamDestroy(p->lane[i]);
+      if (p->din[i]) cudaFree(p->din[i]);
+      if (p->dout[i]) cudaFree(p->dout[i]);
+    }
+    if (p->tables) cudaFree(p->tables);
+  }
+  delete p;
+  return ASX_OK;
+}
+
+int asx_plan_query(asx_plan_t p, asx_plan_info* info) {
+  if (!p || !info) return fail(ASX_ERR_INVALID, "NULL plan or info");
+  std::memset(info, 0, sizeof(*info));
+  info->n = p->n;
+  info->m = p->m;
+  info->a_num = p->a;
+  info->a_den = p->d;
+  info->m_ref = p->m_ref;
+  info->depth = p->depth;
+  info->leaf = p->leaf;
+  info->method = p->method;
+  info->dtype = p->dtype;
+  info->real_input = p->real_input;
+  info->fft_size = p->P;
+  info->predicted_mults = p->pred_mults;
+  info->predicted_adds = p->pred_adds;
+  info->workspace_bytes = (int64_t)p->table_bytes;
+  info->kernels_per_execute = 1;
+  info->device = p->device;
+  return ASX_OK;
+}
+
+int asx_execute(asx_plan_t p, const void* x, int64_t x_stride, void* X, int64_t X_stride, int64_t batch,
+                void* stream) {
+  if (!p) return fail(ASX_ERR_INVALID, "NULL plan");
+  if (batch < 0) return fail(ASX_ERR_INVALID, "batch must be >= 0");
+  if (batch > 0 && (!x || !X)) return fail(ASX_ERR_INVALID, "NULL data pointer");
+  if (x_stride < p->n && batch > 1) return fail(ASX_ERR_INVALID, "x_stride smaller than n");
+  if (X_stride < p->m && batch > 1) return fail(ASX_ERR_INVALID, "X_stride smaller than m");
+  DeviceGuard guard(p->device);
+  if (!guard.ok) return fail(ASX_ERR_CUDA, "cannot select CUDA device");
+  return launch_execute(p, x, x_stride, X, X_stride, batch, static_cast<cudaStream_t>(stream));
+}
+
+int asx_execute_host(asx_plan_t p, const void* x, int64_t x_stride, void* X, int64_t X_stride, int64_t batch,
+                     int64_t chunk) {
+  if (!p) return fail(ASX_ERR_INVALID, "NULL plan");
+  if (batch < 0) return fail(ASX_ERR_INVALID, "batch must be >= 0");
+  if (batch == 0) return ASX_OK;
+  if (!x || !X) return fail(ASX_ERR_INVALID, "NULL data pointer");
+  if (x_stride < p->n || X_stride < p->m) return fail(ASX_ERR_INVALID, "row stride smaller than row length");
+  std::lock_guard<std::mutex> lk(p->host_mtx);
+  DeviceGuard guard(p->device);
+  if (!guard.ok) return fail(ASX_ERR_CUDA, "cannot select CUDA device");
+  const size_t ib = in_elem(p), ob = celem(p->dtype);
+  const size_t in_row = (size_t)p->n * ib, out_row = (size_t)p->m * ob;
+  if (chunk <= 0) chunk = std::max<int64_t>(1, (int64_t)((64ull << 20) / std::max(in_row + out_row, (size_t)1)));
+  chunk = std::min(chunk, batch);
+  if (chunk > p->lane_rows) {
+    for (int i = 0; i < asx_plan_s::kLanes; ++i) {
+      if (p->din[i]) cudaFree(p->din[i]);
+      if (p->dout[i]) cudaFree(p->dout[i]);
+      p->din[i] = p->dout[i] = nullptr;
+    }
+    p->lane_rows = 0;
+    for (int i = 0; i < asx_plan_s::kLanes; ++i) {
+      if (!p->lane[i]) CK(cudaStreamCreateWithFlags(&p->lane[i], cudaStreamNonBlocking));
+      CK(cudaMalloc(&p->din[i], chunk * in_row));
+      CK(cudaMalloc(&p->dout[i], chunk * out_row));
+    }
+    p->lane_rows = chunk;
+  }
+  int k = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, k = (k + 1) % asx_plan_s::kLanes) {
+    const int64_t rows = std::min(chunk, batch - b0);
+    cudaStream_t st = p->lane[k];
+    const char* src = static_cast<const char*>(x) + (size_t)b0 * x_stride * ib;
+    char* dst = static_cast<char*>(X) + (size_t)b0 * X_stride * ob;
+    if ((size_t)x_stride * ib == in_row)
+      CK(cudaMemcpyAsync(p->din[k], src, rows * in_row, cudaMemcpyHostToDevice, st));
+    else
+      CK(cudaMemcpy2DAsync(p->din[k], in_row, src, (size_t)x_stride * ib, in_row, rows, cudaMemcpyHostToDevice,
+                           st));
+    int rc = launch_execute(p, p->din[k], p->n, p->dout[k], p->m, rows, st);
+    if (rc != ASX_OK) return rc;
+    if ((size_t)X_stride * ob == out_row)
+      CK(cudaMemcpyAsync(dst, p->dout[k], rows * out_row, cudaMemcpyDeviceToHost, st));
+    else
+      CK(cudaMemcpy2DAsync(dst, (size_t)X_stride * ob, p->dout[k], out_row, out_row, rows, cudaMemcpyDeviceToHost,
+                           st));
+  }
+  for (int i = 0; i < asx_plan_s::kLanes; ++i) CK(cudaStreamSynchronize(p->lane[i]));
+  return ASX_OK;
+}
+
+int asx_dft_matrix(int64_t n, int64_t a_num, int64_t a_den, int64_t m_rows, int dtype, void* W, void* stream) {
+  if (n < 1 || a_num < 1 || a_den < 1 || m_rows < 0) return fail(ASX_ERR_INVALID, "bad dft_matrix arguments");
+  if (dtype != ASX_C64 && dtype != ASX_C128) return fail(ASX_ERR_INVALID, "bad dtype");
+  if (m_rows == 0) return ASX_OK;
+  if (!W) return fail(ASX_ERR_INVALID, "NULL output");
+  const int64_t g = gcd64(a_num, a_den);
+  const int64_t a = a_num / g, d = a_den / g;
+  const int64_t total = m_rows * n;
+  k_dft_matrix<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0,
+                 static_cast<cudaStream_t>(stream)>>>(W, m_rows, n, (uint64_t)a, (uint64_t)(d * n),
+                                                      dtype == ASX_C128);
+  CK(cudaGetLastError());
+  return ASX_OK;
+}
+
+int asx_combine(const void* y, const void* z, const void* tw, void* out, int64_t rows, int64_t half, int dtype,
+                void* stream) {
+  if (rows < 0 || half < 0) return fail(ASX_ERR_INVALID, "bad combine shape");
+  if (rows * half == 0) return ASX_OK;
+  if (!y || !z || !tw || !out) return fail(ASX_ERR_INVALID, "NULL pointer");
+  const int64_t total = rows * half;
+  const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 65535);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == ASX_C64)
+    k_combine<float><<<blocks, 256, 0, st>>>(y, z, tw, out, rows, half);
+  else if (dtype == ASX_C128)
+    k_combine<double><<<blocks, 256, 0, st>>>(y, z, tw, out, rows, half);
+  else
+    return fail(ASX_ERR_INVALID, "bad dtype");
+  CK(cudaGetLastError());
+  return ASX_OK;
+}
+
+int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype, void* stream) {
+  if (rows < 0 || len < 0) return fail(ASX_ERR_INVALID, "bad block_sum shape");
+  if (rows == 0) return ASX_OK;
+  if (!x || !out) return fail(ASX_ERR_INVALID, "NULL pointer");
+  if (rows > 0x7fffffffLL) return fail(ASX_ERR_INVALID, "too many rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == ASX_C64)
+    k_block_sum<float><<<(unsigned)rows, 256, 0, st>>>(x, out, rows, len);
+  else if (dtype == ASX_C128)
+    k_block_sum<double><<<(unsigned)rows, 256, 0, st>>>(x, out, rows, len);
+  else
+    return fail(ASX_ERR_INVALID, "bad dtype");
+  CK(cudaGetLastError());
+  return ASX_OK;
+}
+
+}  // extern "C"

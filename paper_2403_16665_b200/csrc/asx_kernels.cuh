@@ -1,0 +1,338 @@
+// asx_kernels.cuh — sm_100a kernels of the α-DFT / α-FFT hot path.
+//
+//   k_afft    α-FFT (fastpath.py:130-181), one team per (signal, output residue)
+//   k_chirp   chirp-z factorisation of the same α-DFT, one team per signal
+//   k_direct  direct α-DFT as a tiled complex contraction with W[M,N]
+//             (oracle.py:37-67 _reduced_product, batched)
+//   plan-time table builders (exact integer argument reduction + sincospi,
+//   the device restatement of oracle.py:21-23 roots_of_unity and the
+//   fastpath.py:104-109 twiddle tables)
+//   k_combine / k_block_sum  the reference's building blocks
+//   (fastpath.py:130-151, :154-159)
+#pragma once
+
+#include "asx_engine.cuh"
+
+namespace asx {
+
+struct KParams {
+  const void* x;
+  int64_t xs;  // input row stride (elements)
+  void* X;
+  int64_t Xs;  // output row stride (complex elements)
+  int64_t batch;
+  int64_t n, m;
+  int64_t r;     // afft: output residue classes (alpha = 1/r); 1 when folding
+  int64_t fold;  // afft: folded blocks (alpha = fold, BLOCK_SUM leaf); else 1
+  int real_in;
+  int lfA;             // log2 of the fine part of twA
+  const void* twP;     // two-level W_P table (P = inner FFT size)
+  const void* twA;     // two-level W_{rN} table (α pre-twiddle)
+  const void* chirp;   // chirp[k], k < max(N, M)
+  const void* H;       // chirp kernel spectrum / P, P entries
+  const void* W;       // direct: M x N
+};
+
+template <typename C>
+__device__ __forceinline__ C load_in(const void* x, int64_t idx, int real_in) {
+  using Real = decltype(C{}.x);
+  if (real_in) return mk(__ldg(reinterpret_cast<const Real*>(x) + idx), Real(0));
+  return __ldg(reinterpret_cast<const C*>(x) + idx);
+}
+
+// ---------------------------------------------------------------------------
+// α-FFT, α = 1/r (reference DenseFactor(r): SINGLE_SAMPLE leaf) or α = fold
+// (reference DenseFactor(1, fold): BLOCK_SUM leaf).
+//
+// The reference sweeps the even/odd recursion level-synchronously over the
+// whole r*N-bin spectrum (fastpath.py:162-181), a working set of r*N values
+// per signal.  Splitting the bin index m = c + r*d (c < r) turns the
+// (rN x N) matrix into r independent (N x N) DFTs of the α-twiddled signal
+// x_n * W_{rN}^{c n}, each evaluated by the same radix-2^k even/odd
+// recursion (fastpath.py:130-151 butterflies, grouped Rp levels per pass).
+// Each (signal, c) therefore needs only N values of on-chip state and the
+// outputs with m >= M are never stored (output pruning).
+// ---------------------------------------------------------------------------
+template <typename Real, int P, int NT, int TPB>
+__global__ void __launch_bounds__(NT* TPB) k_afft(KParams p) {
+  using E = Fft<Real, P, NT>;
+  using C = typename CT<Real>::T;
+  constexpr int R = E::R;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / NT) * E::SMEM_ELEMS;
+  const int t = threadIdx.x % NT;
+  const int64_t u = int64_t(blockIdx.x) * TPB + threadIdx.x / NT;
+  const int64_t b = u / p.r, c = u - (u / p.r) * p.r;
+  const bool live = b < p.batch;
+  const C* twP = reinterpret_cast<const C*>(p.twP);
+  const C* twA = reinterpret_cast<const C*>(p.twA);
+
+  C v[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int nn = t + NT * i;
+    C val = mk(Real(0), Real(0));
+    if (live) {
+      const int64_t row = b * p.xs + nn;
+      val = load_in<C>(p.x, row, p.real_in);
+      for (int64_t s = 1; s < p.fold; ++s) val = cadd(val, load_in<C>(p.x, row + s * P, p.real_in));
+      if (c != 0) val = cmul(val, tw_lookup_rt(twA, c * nn, p.lfA));
+    }
+    v[i] = val;
+  }
+  E::run(v, sm, t, twP);
+  if (live) {
+    C* X = reinterpret_cast<C*>(p.X) + b * p.Xs;
+    const int64_t period = p.r * P;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int d = t + NT * i;
+      for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = v[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// chirp-z: a*m*n = a*(m^2 + n^2 - (m-n)^2)/2 turns the α-DFT into
+//   X_m = chirp[m] * sum_n (x_n chirp[n]) * conj(chirp[m-n]),
+//   chirp[k] = exp(-pi*i*((a k^2) mod 2dN)/(dN)),
+// a linear convolution evaluated as a P-point cyclic one (P >= N+M-1):
+// forward FFT, multiply by H = FFT(h)/P, inverse FFT as conj(FFT(conj(.))).
+// The last forward pass and the first inverse pass share the io layout, so
+// the spectrum never leaves registers.
+// ---------------------------------------------------------------------------
+template <typename Real, int P, int NT, int TPB>
+__global__ void __launch_bounds__(NT* TPB) k_chirp(KParams p) {
+  using E = Fft<Real, P, NT>;
+  using C = typename CT<Real>::T;
+  constexpr int R = E::R;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / NT) * E::SMEM_ELEMS;
+  const int t = threadIdx.x % NT;
+  const int64_t b = int64_t(blockIdx.x) * TPB + threadIdx.x / NT;
+  const bool live = b < p.batch;
+  const C* twP = reinterpret_cast<const C*>(p.twP);
+  const C* chirp = reinterpret_cast<const C*>(p.chirp);
+  const C* H = reinterpret_cast<const C*>(p.H);
+
+  C v[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int nn = t + NT * i;
+    C val = mk(Real(0), Real(0));
+    if (live && nn < p.n) val = cmul(load_in<C>(p.x, b * p.xs + nn, p.real_in), __ldg(chirp + nn));
+    v[i] = val;
+  }
+  E::run(v, sm, t, twP);
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = cconj(cmul(v[i], __ldg(H + t + NT * i)));
+  E::run(v, sm, t, twP);
+  if (live) {
+    C* X = reinterpret_cast<C*>(p.X) + b * p.Xs;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int mm = t + NT * i;
+      if (mm < p.m) X[mm] = cmul(cconj(v[i]), __ldg(chirp + mm));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Direct α-DFT: X[b, m] = sum_n x[b, n] * W[m, n], a 64x64 (signals x bins)
+// CTA tile, K-step 16, 4x4 complex micro-tile per thread (FFMA / DFMA).
+// W is the plan's exactly-reduced matrix (oracle.py:26-34 semantics).
+// ---------------------------------------------------------------------------
+template <typename Real>
+__global__ void __launch_bounds__(256) k_direct(KParams p) {
+  using C = typename CT<Real>::T;
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ C xs_t[BK][BM + 1];
+  __shared__ C ws_t[BK][BN + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t b0 = int64_t(blockIdx.y) * BM;
+  const int64_t m0 = int64_t(blockIdx.x) * BN;
+  const C* W = reinterpret_cast<const C*>(p.W);
+  C acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = mk(Real(0), Real(0));
+
+  for (int64_t k0 = 0; k0 < p.n; k0 += BK) {
+#pragma unroll
+    for (int e = 0; e < (BM * BK) / 256; ++e) {
+      const int idx = tid + 256 * e;
+      const int s = idx / BK, k = idx % BK;
+      const int64_t bb = b0 + s, kk = k0 + k;
+      C val = mk(Real(0), Real(0));
+      if (bb < p.batch && kk < p.n) val = load_in<C>(p.x, bb * p.xs + kk, p.real_in);
+      xs_t[k][s] = val;
+      const int64_t mm = m0 + s;
+      C w = mk(Real(0), Real(0));
+      if (mm < p.m && kk < p.n) w = __ldg(W + mm * p.n + kk);
+      ws_t[k][s] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      C a[4], w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = xs_t[k][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = ws_t[k][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j].x = fma(a[i].x, w[j].x, fma(-a[i].y, w[j].y, acc[i][j].x));
+          acc[i][j].y = fma(a[i].x, w[j].y, fma(a[i].y, w[j].x, acc[i][j].y));
+        }
+    }
+    __syncthreads();
+  }
+  C* X = reinterpret_cast<C*>(p.X);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t bb = b0 + ty + 16 * i;
+    if (bb >= p.batch) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t mm = m0 + tx + 16 * j;
+      if (mm < p.m) X[bb * p.Xs + mm] = acc[i][j];
+    }
+  }
+}
+
+// ----------------------------- plan-time tables ----------------------------
+
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t L) {
+  return (uint64_t)(((unsigned __int128)a * b) % L);
+}
+
+__device__ __forceinline__ void store_c(void* out, int64_t i, double re, double im, int dbl) {
+  if (dbl)
+    reinterpret_cast<double2*>(out)[i] = make_double2(re, im);
+  else
+    reinterpret_cast<float2*>(out)[i] = make_float2((float)re, (float)im);
+}
+
+// out[k] = W_L^{(k*step) mod L} = exp(-2*pi*i*((k*step) mod L)/L), k < count.
+__global__ void k_fill_roots(void* out, int64_t count, uint64_t step, uint64_t L, int dbl) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t j = mulmod((uint64_t)k, step, L);
+    double s, c;
+    sincospi(2.0 * (double)j / (double)L, &s, &c);
+    store_c(out, k, c, -s, dbl);
+  }
+}
+
+// out[k] = exp(-pi*i*((a*k^2) mod L2)/(L2/2)), L2 = 2*d*N.
+__global__ void k_fill_chirp(void* out, int64_t count, uint64_t a, uint64_t L2, int dbl) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t kk = mulmod((uint64_t)k, (uint64_t)k, L2);
+    const uint64_t j = mulmod(kk, a, L2);
+    double s, c;
+    sincospi(2.0 * (double)j / (double)L2, &s, &c);
+    store_c(out, k, c, -s, dbl);
+  }
+}
+
+// H[k] = (1/P) sum_j h[j] W_P^{jk}, h[j] = conj(chirp[j]) (j < M),
+// conj(chirp[P-j]) (P-j < N), else 0.  Direct O(P^2) summation in FP64 with
+// an exact W_P table (plan-time only).
+__global__ void k_chirp_spectrum(void* out, int P, int64_t n, int64_t m, uint64_t a, uint64_t L2,
+                                 const double2* __restrict__ wP, int dbl) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P) return;
+  double accx = 0.0, accy = 0.0;
+  for (int j = 0; j < P; ++j) {
+    int64_t src;
+    if (j < m)
+      src = j;
+    else if (P - j < n)
+      src = P - j;
+    else
+      continue;
+    const uint64_t kk = mulmod((uint64_t)src, (uint64_t)src, L2);
+    const uint64_t jj = mulmod(kk, a, L2);
+    double s, c;
+    sincospi(2.0 * (double)jj / (double)L2, &s, &c);
+    // h = conj(chirp) = (c, +s)
+    const double2 w = __ldg(wP + (((uint64_t)j * (uint64_t)k) & (uint64_t)(P - 1)));
+    accx += c * w.x - s * w.y;
+    accy += c * w.y + s * w.x;
+  }
+  store_c(out, k, accx / P, accy / P, dbl);
+}
+
+// W[r, c] = W_L^{(a*r*c) mod L}, L = d*n, row-major rows x n.
+__global__ void k_dft_matrix(void* out, int64_t rows, int64_t n, uint64_t a, uint64_t L, int dbl) {
+  const int64_t total = rows * n;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / n, c = i % n;
+    const uint64_t j = mulmod(mulmod(a, r, L), c, L);
+    double s, cc;
+    sincospi(2.0 * (double)j / (double)L, &s, &cc);
+    store_c(out, i, cc, -s, dbl);
+  }
+}
+
+// ------------------------- reference building blocks -----------------------
+
+template <typename Real>
+__global__ void k_combine(const void* y, const void* z, const void* tw, void* out, int64_t rows,
+                          int64_t half) {
+  using C = typename CT<Real>::T;
+  const C* Y = reinterpret_cast<const C*>(y);
+  const C* Z = reinterpret_cast<const C*>(z);
+  const C* T = reinterpret_cast<const C*>(tw);
+  C* O = reinterpret_cast<C*>(out);
+  const int64_t total = rows * half;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / half, l = i % half;
+    const C t = cmul(__ldg(T + l), __ldg(Z + i));
+    const C yy = __ldg(Y + i);
+    O[r * 2 * half + l] = cadd(yy, t);
+    O[r * 2 * half + half + l] = csub(yy, t);
+  }
+}
+
+template <typename Real>
+__global__ void k_block_sum(const void* x, void* out, int64_t rows, int64_t len) {
+  using C = typename CT<Real>::T;
+  const C* Xp = reinterpret_cast<const C*>(x);
+  C* O = reinterpret_cast<C*>(out);
+  const int64_t row = blockIdx.x;
+  if (row >= rows) return;
+  Real sx = 0, sy = 0;
+  for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
+    const C v = __ldg(Xp + row * len + j);
+    sx += v.x;
+    sy += v.y;
+  }
+  __shared__ Real red[2][32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_down_sync(0xffffffffu, sx, o);
+    sy += __shfl_down_sync(0xffffffffu, sy, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = sx;
+    red[1][threadIdx.x >> 5] = sy;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Real ax = 0, ay = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      ax += red[0][w];
+      ay += red[1][w];
+    }
+    O[row] = mk(ax, ay);
+  }
+}
+
+}  // namespace asx
