@@ -15,6 +15,10 @@ $(PKG)/libasx.so: | build
 build:
 	mkdir -p build
 
+# performance variants for tuning sweeps (scripts/sweep.py with ASX_LIB_PATH)
+variant: | build
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -shared -o $(PKG)/libasx_$(VNAME).so $(SRC) 2> build/ptxas_$(VNAME).log
+
 clean:
 	rm -f $(PKG)/libasx.so
 

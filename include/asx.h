@@ -133,6 +133,10 @@ int asx_combine(const void* y, const void* z, const void* tw, void* out, int64_t
 int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype,
                   void* stream);
 
+/* Launch shape of the last FFT-family kernel this thread launched: grid,
+ * block, dynamic shared memory and whether rows were TMA-staged. */
+int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged);
+
 const char* asx_strerror(int status);
 /* Message of the last failing call on this thread ("" if none). */
 const char* asx_last_error(void);

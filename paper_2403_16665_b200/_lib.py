@@ -12,7 +12,7 @@ import os
 
 from .core import UnsupportedSizeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libasx.so")
+LIB_PATH = os.environ.get("ASX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libasx.so")
 
 ASX_OK = 0
 ASX_ERR_INVALID = 2
@@ -70,6 +70,7 @@ SIGNATURES = {
     "asx_dft_matrix": (ctypes.c_int, [_I64, _I64, _I64, _I64, ctypes.c_int, _VP, _VP]),
     "asx_combine": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _I64, ctypes.c_int, _VP]),
     "asx_block_sum": (ctypes.c_int, [_VP, _VP, _I64, _I64, ctypes.c_int, _VP]),
+    "asx_last_launch": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 4),
     "asx_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "asx_last_error": (ctypes.c_char_p, []),
 }

@@ -65,6 +65,18 @@ int bit_length(int64_t v) {
 constexpr int kMaxP_c64 = 16384;
 constexpr int kMaxP_c128 = 8192;
 
+struct LaunchEnv {
+  int sms = 148;
+  size_t smem_optin = 227 * 1024;
+};
+
+// Shape of the most recent launch on this thread (asx_last_launch, for
+// benchmarks / tests that report occupancy decisions).
+struct LastLaunch {
+  int grid = 0, block = 0, smem = 0, staged = 0;
+};
+thread_local LastLaunch g_last_launch;
+
 }  // namespace
 
 struct asx_plan_s {
@@ -80,6 +92,8 @@ struct asx_plan_s {
   size_t table_bytes = 0;
   size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
   int lfA = 0;
+  int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
+  LaunchEnv env;
   // execute_host resources
   std::mutex host_mtx;
   static constexpr int kLanes = 3;
@@ -99,12 +113,34 @@ size_t in_elem(const asx_plan_s* p) {
 
 // --------------------------- kernel dispatch --------------------------------
 
+// Team shape per (precision, FFT size): R values per thread, NT = P/R
+// threads per transform, TPB transforms per CTA.  Chosen so the data fits the
+// register budget at the CTA size (no spills, see build/ptxas.log).
+#ifndef ASX_R_BIG_C64
+#define ASX_R_BIG_C64 16  // values per thread for c64 P >= 4096
+#endif
+#ifndef ASX_R_16K_C64
+#define ASX_R_16K_C64 16  // values per thread for c64 P == 16384
+#endif
+#ifndef ASX_R_4K_C128
+#define ASX_R_4K_C128 8  // values per thread for c128 P == 4096
+#endif
+#ifndef ASX_MT_C64
+#define ASX_MT_C64 1024  // threads per SM the register budget targets (c64)
+#endif
+#ifndef ASX_MT_C128
+#define ASX_MT_C128 512  // threads per SM the register budget targets (c128)
+#endif
 template <int P, typename Real> struct Cfg {
-  static constexpr int R = (P <= 32) ? P : ((P >= 16384) ? 32 : 16);
+  static constexpr bool DBL = sizeof(Real) == 8;
+  static constexpr int R = (P <= 32)     ? P
+                           : (P <= 2048) ? 8
+                           : DBL         ? (P == 4096 ? ASX_R_4K_C128 : 16)
+                                         : (P == 16384 ? ASX_R_16K_C64 : ASX_R_BIG_C64);
   static constexpr int NT = P / R;
-  static constexpr int TPB = (NT >= 256) ? 1 : (NT == 1 ? 64 : 256 / NT);
-  using E = Fft<Real, P, NT>;
-  static constexpr size_t SMEM = size_t(TPB) * E::SMEM_ELEMS * sizeof(typename CT<Real>::T);
+  static constexpr int TPB = (NT == 1) ? 64 : (NT >= 256 ? 1 : 256 / NT);
+  static constexpr int MT = DBL ? ASX_MT_C128 : ASX_MT_C64;
+  static constexpr int MINB = (MT / (NT * TPB)) > 1 ? (MT / (NT * TPB)) : 1;
 };
 
 template <typename KernelT>
@@ -113,32 +149,78 @@ cudaError_t prep_smem(KernelT kern, size_t smem) {
   return cudaSuccess;
 }
 
-template <typename Real, int P>
-cudaError_t launch_fft_family(int which, const KParams& kp, int64_t units, cudaStream_t st) {
+template <typename Real, int P, int KIND>
+cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const LaunchEnv& env) {
   using G = Cfg<P, Real>;
-  const int64_t blocks = (units + G::TPB - 1) / G::TPB;
-  if (blocks == 0) return cudaSuccess;
-  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  if (which == ASX_FFT) {
-    auto kern = k_afft<Real, P, G::NT, G::TPB>;
-    cudaError_t e = prep_smem(kern, G::SMEM);
+  using L = PersistLayout<Real, P, G::NT, G::TPB>;
+  if (batch == 0) return cudaSuccess;
+  const size_t row_bytes = size_t(kp.n) * (kp.real_in ? sizeof(Real) : 2 * sizeof(Real));
+  auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB>;
+  // one-time opt-in to the full shared-memory carve-out for this kernel
+  static thread_local int attr_set_for = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_set_for != dev) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)blocks, G::NT * G::TPB, G::SMEM, st>>>(kp);
-  } else {
-    auto kern = k_chirp<Real, P, G::NT, G::TPB>;
-    cudaError_t e = prep_smem(kern, G::SMEM);
-    if (e != cudaSuccess) return e;
-    kern<<<(unsigned)blocks, G::NT * G::TPB, G::SMEM, st>>>(kp);
+    attr_set_for = dev;
   }
+  // occupancy with / without the TMA staging buffer (cached per smem size);
+  // staging is used only when it does not cost resident CTAs.
+  struct Occ {
+    size_t smem = 0;
+    int per_sm = 0;
+  };
+  static thread_local Occ cache[2];
+  auto occ = [&](int stg, size_t sm) -> int {
+    if (sm > env.smem_optin) return 0;
+    Occ& c = cache[stg];
+    if (c.smem != sm) {
+      int v = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, G::NT * G::TPB, sm) != cudaSuccess) {
+        cudaGetLastError();
+        v = 0;
+      }
+      c.smem = sm;
+      c.per_sm = v;
+    }
+    return c.per_sm;
+  };
+  if (G::NT == 1) kp.staged = 0;
+  const size_t smem_u = L::total(row_bytes, false, kp.tw_elems);
+  const int occ_u = occ(0, smem_u);
+  size_t smem = smem_u;
+  int per_sm = occ_u;
+  if (kp.staged) {
+    const size_t smem_s = L::total(row_bytes, true, kp.tw_elems);
+    const int occ_s = occ(1, smem_s);
+    if (occ_s >= occ_u && occ_s > 0) {
+      smem = smem_s;
+      per_sm = occ_s;
+    } else {
+      kp.staged = 0;
+    }
+  }
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int64_t need = (batch + G::TPB - 1) / G::TPB;
+  const int64_t grid = std::min<int64_t>(need, int64_t(env.sms) * per_sm);
+  kp.batch = batch;
+  kern<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
+  g_last_launch.grid = (int)grid;
+  g_last_launch.block = G::NT * G::TPB;
+  g_last_launch.smem = (int)smem;
+  g_last_launch.staged = kp.staged;
   return cudaGetLastError();
 }
 
 template <typename Real>
-cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t units, cudaStream_t st) {
+cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t batch, cudaStream_t st,
+                           const LaunchEnv& env) {
   switch (P) {
-#define ASX_CASE(S) \
-  case S:           \
-    return launch_fft_family<Real, S>(which, kp, units, st);
+#define ASX_CASE(S)                                                               \
+  case S:                                                                         \
+    return which == ASX_FFT ? launch_persist<Real, S, KIND_AFFT>(kp, batch, st, env) \
+                            : launch_persist<Real, S, KIND_CHIRP>(kp, batch, st, env);
     ASX_CASE(1)
     ASX_CASE(2)
     ASX_CASE(4)
@@ -155,7 +237,9 @@ cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t units, c
     ASX_CASE(8192)
 #undef ASX_CASE
     case 16384:
-      if constexpr (sizeof(Real) == 4) return launch_fft_family<Real, 16384>(which, kp, units, st);
+      if constexpr (sizeof(Real) == 4)
+        return which == ASX_FFT ? launch_persist<Real, 16384, KIND_AFFT>(kp, batch, st, env)
+                                : launch_persist<Real, 16384, KIND_CHIRP>(kp, batch, st, env);
       return cudaErrorInvalidValue;
     default:
       return cudaErrorInvalidValue;
@@ -214,6 +298,7 @@ void fill_kparams(const asx_plan_s* p, KParams& kp) {
   kp.chirp = base + p->off_chirp;
   kp.H = base + p->off_H;
   kp.W = base + p->off_W;
+  kp.tw_elems = p->tw_elems;
 }
 
 int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs, int64_t batch,
@@ -252,11 +337,15 @@ int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int6
     }
     e = cudaGetLastError();
   } else {
-    const int64_t units = (p->method == ASX_FFT) ? batch * p->r : batch;
+    const size_t ie = in_elem(p);
+    kp.staged = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && ((size_t)xs * ie) % 16 == 0 &&
+                 ((size_t)p->n * ie) % 16 == 0 && (batch == 1 || xs >= p->n))
+                    ? 1
+                    : 0;
     if (p->dtype == ASX_C64)
-      e = launch_by_size<float>(p->method, p->P, kp, units, st);
+      e = launch_by_size<float>(p->method, p->P, kp, batch, st, p->env);
     else
-      e = launch_by_size<double>(p->method, p->P, kp, units, st);
+      e = launch_by_size<double>(p->method, p->P, kp, batch, st, p->env);
   }
   if (e != cudaSuccess) return cuda_fail(e, "asx_execute launch");
   return ASX_OK;
@@ -283,6 +372,14 @@ const char* asx_strerror(int status) {
 }
 
 const char* asx_last_error(void) { return g_last_error.c_str(); }
+
+int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged) {
+  if (grid) *grid = g_last_launch.grid;
+  if (block) *block = g_last_launch.block;
+  if (smem_bytes) *smem_bytes = g_last_launch.smem;
+  if (staged) *staged = g_last_launch.staged;
+  return ASX_OK;
+}
 
 int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, int64_t m, int dtype,
                     int real_input, int method, int device) {
@@ -382,6 +479,13 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     delete p;
     return fail(ASX_ERR_CUDA, "cannot select CUDA device " + std::to_string(device) + " (no GPU?)");
   }
+  {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) p->env.sms = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)
+      p->env.smem_optin = (size_t)v;
+    cudaGetLastError();
+  }
   const int dbl = dtype == ASX_C128;
   const size_t es = celem(dtype);
   // ---- table layout ----
@@ -410,6 +514,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     H_sz = p->P;
   }
   if (chosen == ASX_DIRECT) W_sz = m * n;
+  p->tw_elems = (int)twA_sz;  // shared-memory table: α pre-twiddle only
   auto align = [](size_t v) { return (v + 31) & ~size_t(31); };
   p->off_twP = 0;
   elems = align(twP_sz);

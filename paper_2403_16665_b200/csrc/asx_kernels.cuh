@@ -31,6 +31,8 @@ struct KParams {
   const void* chirp;   // chirp[k], k < max(N, M)
   const void* H;       // chirp kernel spectrum / P, P entries
   const void* W;       // direct: M x N
+  int staged;          // 1: rows fetched by TMA into shared memory
+  int tw_elems;        // shared twiddle elements (W_P two-level [+ W_rN two-level])
 };
 
 template <typename C>
@@ -40,99 +42,205 @@ __device__ __forceinline__ C load_in(const void* x, int64_t idx, int real_in) {
   return __ldg(reinterpret_cast<const C*>(x) + idx);
 }
 
-// ---------------------------------------------------------------------------
-// α-FFT, α = 1/r (reference DenseFactor(r): SINGLE_SAMPLE leaf) or α = fold
-// (reference DenseFactor(1, fold): BLOCK_SUM leaf).
-//
-// The reference sweeps the even/odd recursion level-synchronously over the
-// whole r*N-bin spectrum (fastpath.py:162-181), a working set of r*N values
-// per signal.  Splitting the bin index m = c + r*d (c < r) turns the
-// (rN x N) matrix into r independent (N x N) DFTs of the α-twiddled signal
-// x_n * W_{rN}^{c n}, each evaluated by the same radix-2^k even/odd
-// recursion (fastpath.py:130-151 butterflies, grouped Rp levels per pass).
-// Each (signal, c) therefore needs only N values of on-chip state and the
-// outputs with m >= M are never stored (output pruning).
-// ---------------------------------------------------------------------------
-template <typename Real, int P, int NT, int TPB>
-__global__ void __launch_bounds__(NT* TPB) k_afft(KParams p) {
-  using E = Fft<Real, P, NT>;
-  using C = typename CT<Real>::T;
-  constexpr int R = E::R;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / NT) * E::SMEM_ELEMS;
-  const int t = threadIdx.x % NT;
-  const int64_t u = int64_t(blockIdx.x) * TPB + threadIdx.x / NT;
-  const int64_t b = u / p.r, c = u - (u / p.r) * p.r;
-  const bool live = b < p.batch;
-  const C* twP = reinterpret_cast<const C*>(p.twP);
-  const C* twA = reinterpret_cast<const C*>(p.twA);
-
-  C v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int nn = t + NT * i;
-    C val = mk(Real(0), Real(0));
-    if (live) {
-      const int64_t row = b * p.xs + nn;
-      val = load_in<C>(p.x, row, p.real_in);
-      for (int64_t s = 1; s < p.fold; ++s) val = cadd(val, load_in<C>(p.x, row + s * P, p.real_in));
-      if (c != 0) val = cmul(val, tw_lookup_rt(twA, c * nn, p.lfA));
-    }
-    v[i] = val;
+// Input sample n of the staged row (shared memory) or straight from global.
+template <typename C>
+__device__ __forceinline__ C load_row(const unsigned char* stage, const void* x, int64_t row_off, int64_t n,
+                                      int real_in, bool staged) {
+  using Real = decltype(C{}.x);
+  if (staged) {
+    if (real_in) return mk(reinterpret_cast<const Real*>(stage)[n], Real(0));
+    return reinterpret_cast<const C*>(stage)[n];
   }
-  E::run(v, sm, t, twP);
-  if (live) {
-    C* X = reinterpret_cast<C*>(p.X) + b * p.Xs;
-    const int64_t period = p.r * P;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int d = t + NT * i;
-      for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = v[i];
-    }
-  }
+  return load_in<C>(x, row_off + n, real_in);
 }
 
-// ---------------------------------------------------------------------------
-// chirp-z: a*m*n = a*(m^2 + n^2 - (m-n)^2)/2 turns the α-DFT into
-//   X_m = chirp[m] * sum_n (x_n chirp[n]) * conj(chirp[m-n]),
-//   chirp[k] = exp(-pi*i*((a k^2) mod 2dN)/(dN)),
-// a linear convolution evaluated as a P-point cyclic one (P >= N+M-1):
-// forward FFT, multiply by H = FFT(h)/P, inverse FFT as conj(FFT(conj(.))).
-// The last forward pass and the first inverse pass share the io layout, so
-// the spectrum never leaves registers.
-// ---------------------------------------------------------------------------
+// Compiler-only fence: keeps the scheduler from hoisting every table load of an
+// unrolled loop at once (which would double live registers and spill).
+__device__ __forceinline__ void reg_fence() { asm volatile("" ::: "memory"); }
+
+__host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Shared-memory layout of the persistent FFT-family kernels (host and device
+// agree on it through this helper).
 template <typename Real, int P, int NT, int TPB>
-__global__ void __launch_bounds__(NT* TPB) k_chirp(KParams p) {
+struct PersistLayout {
   using E = Fft<Real, P, NT>;
   using C = typename CT<Real>::T;
+  static constexpr size_t FFT_BYTES = align_up(size_t(TPB) * E::SMEM_ELEMS * sizeof(C), 128);
+  __host__ __device__ static size_t stage_bytes(size_t row_bytes, bool staged) {
+    return staged ? align_up(row_bytes, 128) : 0;
+  }
+  __host__ __device__ static size_t tw_off(size_t row_bytes, bool staged) {
+    return FFT_BYTES + size_t(TPB) * stage_bytes(row_bytes, staged);
+  }
+  __host__ __device__ static size_t total(size_t row_bytes, bool staged, size_t tw_elems) {
+    return align_up(tw_off(row_bytes, staged) + tw_elems * sizeof(C), 16) + TPB * sizeof(uint64_t);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Persistent FFT-family kernel: each NT-thread team walks its signals
+// u = blockIdx.x*TPB + team, += gridDim.x*TPB.  The next signal's row is
+// fetched global -> shared by a TMA bulk copy (cp.async.bulk + mbarrier)
+// while the current one is transformed; twiddle tables live in shared
+// memory; results leave registers straight to HBM in the io layout.
+//
+// KIND_AFFT — α-FFT, α = 1/r (reference DenseFactor(r), SINGLE_SAMPLE leaf)
+// or α = fold (DenseFactor(1, fold), BLOCK_SUM leaf).  The reference sweeps
+// the even/odd recursion level-synchronously over the whole r*N-bin
+// spectrum (fastpath.py:162-181), a working set of r*N values per signal.
+// Splitting the bin index m = c + r*d (c < r) turns the (rN x N) matrix into
+// r independent (N x N) DFTs of the α-twiddled signal x_n * W_{rN}^{c n},
+// each evaluated by the same radix-2^k even/odd recursion (fastpath.py:
+// 130-151 butterflies, Rp levels fused per pass), so a team needs only N
+// values of state and bins m >= M are never stored.
+//
+// KIND_CHIRP — chirp-z: a*m*n = a*(m^2 + n^2 - (m-n)^2)/2 turns the α-DFT into
+//   X_m = chirp[m] * sum_n (x_n chirp[n]) * conj(chirp[m-n]),
+//   chirp[k] = exp(-pi*i*((a k^2) mod 2dN)/(dN)),
+// a linear convolution done as a P-point cyclic one (P >= N+M-1): forward
+// FFT, multiply by H = FFT(h)/P, inverse FFT as conj(FFT(conj(.))).  The
+// last forward pass and the first inverse pass share the io layout, so the
+// spectrum never leaves registers.
+// ---------------------------------------------------------------------------
+enum { KIND_AFFT = 0, KIND_CHIRP = 1 };
+
+template <typename Real, int P, int NT, int TPB, int KIND, int MINB>
+__global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
+  using E = Fft<Real, P, NT>;
+  using L = PersistLayout<Real, P, NT, TPB>;
+  using C = typename CT<Real>::T;
   constexpr int R = E::R;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / NT) * E::SMEM_ELEMS;
-  const int t = threadIdx.x % NT;
-  const int64_t b = int64_t(blockIdx.x) * TPB + threadIdx.x / NT;
-  const bool live = b < p.batch;
-  const C* twP = reinterpret_cast<const C*>(p.twP);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int team = threadIdx.x / NT, t = threadIdx.x % NT;
+  const bool staged = p.staged != 0;
+  const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(Real) : sizeof(C));
+  C* fbuf = reinterpret_cast<C*>(smraw) + team * E::SMEM_ELEMS;
+  unsigned char* stage = smraw + L::FFT_BYTES + team * L::stage_bytes(row_bytes, staged);
+  C* twa = reinterpret_cast<C*>(smraw + L::tw_off(row_bytes, staged));  // α pre-twiddle W_{rN} (afft, r > 1)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(
+                      smraw + align_up(L::tw_off(row_bytes, staged) + p.tw_elems * sizeof(C), 16)) + team;
+
+  // per-thread pass twiddles -> registers; α pre-twiddle table -> shared
+  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP));
+  {
+    const C* srca = reinterpret_cast<const C*>(p.twA);
+    for (int i = threadIdx.x; i < p.tw_elems; i += NT * TPB) twa[i] = __ldg(srca + i);
+  }
+  const int64_t stride = int64_t(gridDim.x) * TPB;
+  int64_t u = int64_t(blockIdx.x) * TPB + team;
+  const int64_t iters = (p.batch + stride - 1) / stride;
+  if (staged && t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (staged && t == 0 && u < p.batch) {
+    mbar_expect_tx(bar, (uint32_t)row_bytes);
+    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + u * p.xs * (row_bytes / p.n), (uint32_t)row_bytes,
+                bar);
+  }
+  uint32_t phase = 0;
   const C* chirp = reinterpret_cast<const C*>(p.chirp);
   const C* H = reinterpret_cast<const C*>(p.H);
 
-  C v[R];
+  for (int64_t it = 0; it < iters; ++it, u += stride) {
+    const bool live = u < p.batch;
+    const int64_t row_off = u * p.xs;
+    if constexpr (KIND == KIND_CHIRP) {
+      C v[R];
+      if (staged && live) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+      }
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int nn = t + NT * i;
-    C val = mk(Real(0), Real(0));
-    if (live && nn < p.n) val = cmul(load_in<C>(p.x, b * p.xs + nn, p.real_in), __ldg(chirp + nn));
-    v[i] = val;
-  }
-  E::run(v, sm, t, twP);
+      for (int i = 0; i < R; ++i) {
+        const int nn = t + NT * i;
+        C val = mk(Real(0), Real(0));
+        if (live && nn < p.n) val = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), __ldg(chirp + nn));
+        v[i] = val;
+        if ((i & 3) == 3) reg_fence();
+      }
+      if (staged) {
+        __syncthreads();  // the whole row has been consumed
+        if (t == 0 && u + stride < p.batch) {
+          fence_proxy_async();
+          mbar_expect_tx(bar, (uint32_t)row_bytes);
+          tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + (u + stride) * p.xs * (row_bytes / p.n),
+                      (uint32_t)row_bytes, bar);
+        }
+      }
+      // forward FFT, pointwise kernel spectrum, inverse FFT: one FFT body in
+      // a 2-trip loop so only one copy of the transform is register-allocated
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        E::run(v, fbuf, t, tr);
+        if (half == 0) {
 #pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = cconj(cmul(v[i], __ldg(H + t + NT * i)));
-  E::run(v, sm, t, twP);
-  if (live) {
-    C* X = reinterpret_cast<C*>(p.X) + b * p.Xs;
+          for (int i = 0; i < R; ++i) {
+            v[i] = cconj(cmul(v[i], __ldg(H + t + NT * i)));
+            if ((i & 3) == 3) reg_fence();
+          }
+        }
+      }
+      if (live) {
+        C* X = reinterpret_cast<C*>(p.X) + u * p.Xs;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int mm = t + NT * i;
-      if (mm < p.m) X[mm] = cmul(cconj(v[i]), __ldg(chirp + mm));
+        for (int i = 0; i < R; ++i) {
+          const int mm = t + NT * i;
+          if (mm < p.m) X[mm] = cmul(cconj(v[i]), __ldg(chirp + mm));
+          if ((i & 3) == 3) reg_fence();
+        }
+      }
+    } else {
+      if (staged && live) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+      }
+      for (int c = 0; c < p.r; ++c) {
+        C v[R];
+        // W_{rN}^{c n}, n = t + NT*i: base W^{c t} times step W^{c NT} chained
+        // over i, re-seeded from the shared table every 4 steps.
+        C wst = mk(Real(1), Real(0)), wc = wst;
+        if (c != 0) {
+          wst = tw_lookup_rt(twa, c * NT, p.lfA);
+          wc = tw_lookup_rt(twa, c * t, p.lfA);
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int nn = t + NT * i;
+          C val = mk(Real(0), Real(0));
+          if (live) {
+            val = load_row<C>(stage, p.x, row_off, nn, p.real_in, staged);
+            for (int s = 1; s < p.fold; ++s)
+              val = cadd(val, load_row<C>(stage, p.x, row_off, nn + int64_t(s) * P, p.real_in, staged));
+          }
+          if (c != 0) {
+            if (i > 0) wc = ((i & 3) == 0) ? tw_lookup_rt(twa, c * nn, p.lfA) : cmul(wc, wst);
+            val = cmul(val, wc);
+          }
+          v[i] = val;
+        }
+        if (staged && c == p.r - 1) {
+          __syncthreads();
+          if (t == 0 && u + stride < p.batch) {
+            fence_proxy_async();
+            mbar_expect_tx(bar, (uint32_t)row_bytes);
+            tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + (u + stride) * p.xs * (row_bytes / p.n),
+                        (uint32_t)row_bytes, bar);
+          }
+        }
+        E::run(v, fbuf, t, tr);
+        if (live) {
+          C* X = reinterpret_cast<C*>(p.X) + u * p.Xs;
+          const int64_t period = p.r * P;
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            const int d = t + NT * i;
+            for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = v[i];
+          }
+        }
+      }
     }
   }
 }
