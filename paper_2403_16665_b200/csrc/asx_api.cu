@@ -14,7 +14,7 @@
 #include <string>
 
 #include "../../include/asx.h"
-#include "asx_kernels.cuh"
+#include "asx_large.cuh"
 
 using namespace asx;
 
@@ -93,6 +93,11 @@ struct asx_plan_s {
   size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
   int lfA = 0;
   int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
+  // large chirp path (P > one CTA): four-step P = P1 x P2 through workspace A
+  int large = 0;
+  int64_t P1 = 0, P2 = 0;
+  int lfBig = 0;
+  size_t off_twP1 = 0, off_twBig = 0, off_A = 0;
   LaunchEnv env;
   // execute_host resources
   std::mutex host_mtx;
@@ -246,6 +251,73 @@ cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t batch, c
   }
 }
 
+template <typename Real, int P1>
+cudaError_t launch_cols(int mode, const LParams& lp, cudaStream_t st) {
+  using G = ColCfg<Real, P1>;
+  const unsigned grid = (unsigned)(lp.P2 / kColTile);
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kern) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    if (e == cudaSuccess) kern<<<grid, G::NT * kColTile, G::SMEM, st>>>(lp);
+  };
+  if (mode == COL_FWD_SIGNAL)
+    go(k_large_cols<Real, P1, G::NT, COL_FWD_SIGNAL>);
+  else if (mode == COL_FWD_TABLE)
+    go(k_large_cols<Real, P1, G::NT, COL_FWD_TABLE>);
+  else
+    go(k_large_cols<Real, P1, G::NT, COL_INV_OUT>);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t launch_cols_p1(int64_t P1, int mode, const LParams& lp, cudaStream_t st) {
+  switch (P1) {
+#define ASX_COL(S) \
+  case S:          \
+    return launch_cols<Real, S>(mode, lp, st);
+    ASX_COL(2)
+    ASX_COL(4)
+    ASX_COL(8)
+    ASX_COL(16)
+    ASX_COL(32)
+    ASX_COL(64)
+    ASX_COL(128)
+    ASX_COL(256)
+    ASX_COL(512)
+    ASX_COL(1024)
+#undef ASX_COL
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+template <typename Real>
+cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st) {
+  constexpr int P2 = sizeof(Real) == 4 ? 16384 : 8192;
+  using G = Cfg<P2, Real>;
+  using E = Fft<Real, P2, G::NT>;
+  const size_t smem = size_t(E::SMEM_ELEMS) * sizeof(typename CT<Real>::T);
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kern) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) kern<<<(unsigned)P1, G::NT, smem, st>>>(lp);
+  };
+  if (mode == ROW_SPECTRUM)
+    go(k_large_rows<Real, P2, G::NT, ROW_SPECTRUM>);
+  else
+    go(k_large_rows<Real, P2, G::NT, ROW_MAIN>);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_large(int dbl, int64_t P1, int mode_cols, int mode_rows, int which, const LParams& lp,
+                         cudaStream_t st) {
+  // which: 0 = cols, 1 = rows
+  if (which == 0) return dbl ? launch_cols_p1<double>(P1, mode_cols, lp, st) : launch_cols_p1<float>(P1, mode_cols, lp, st);
+  return dbl ? launch_rows<double>(mode_rows, P1, lp, st) : launch_rows<float>(mode_rows, P1, lp, st);
+}
+
 int two_level_lf(int64_t L) { return (log2i(L) + 1) / 2; }
 
 // Builds [fine(F) | coarse(ceil(L/F))] for W_L at dst.
@@ -336,6 +408,31 @@ int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int6
         k_direct<double><<<grid, 256, 0, st>>>(kp);
     }
     e = cudaGetLastError();
+  } else if (p->large) {
+    char* base = static_cast<char*>(p->tables);
+    LParams lp;
+    std::memset(&lp, 0, sizeof(lp));
+    lp.real_in = p->real_input;
+    lp.n = p->n;
+    lp.m = p->m;
+    lp.chirp = base + p->off_chirp;
+    lp.A = base + p->off_A;
+    lp.Ht = base + p->off_H;
+    lp.twP1 = base + p->off_twP1;
+    lp.twP2 = base + p->off_twP;
+    lp.twBig = base + p->off_twBig;
+    lp.lfBig = p->lfBig;
+    lp.P = p->P;
+    lp.P2 = p->P2;
+    const int dbl = p->dtype == ASX_C128;
+    const size_t ie = in_elem(p), oe = celem(p->dtype);
+    for (int64_t b = 0; b < batch && e == cudaSuccess; ++b) {
+      lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
+      lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
+      e = launch_large(dbl, p->P1, COL_FWD_SIGNAL, 0, 0, lp, st);
+      if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_MAIN, 1, lp, st);
+      if (e == cudaSuccess) e = launch_large(dbl, p->P1, COL_INV_OUT, 0, 0, lp, st);
+    }
   } else {
     const size_t ie = in_elem(p);
     kp.staged = ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && ((size_t)xs * ie) % 16 == 0 &&
@@ -423,7 +520,9 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     fft_P = n / a;
   }
   const int64_t chirp_P = next_pow2(n + m - 1);
-  const bool chirp_ok = chirp_P <= maxP;
+  // one CTA per transform up to maxP; beyond, the four-step path P = P1 x maxP
+  const bool chirp_large = chirp_P > maxP && chirp_P / maxP <= 1024;
+  const bool chirp_ok = chirp_P <= maxP || chirp_large;
 
   auto lg = [](int64_t v) { return (double)std::max(1, log2i(v)); };
   const double cost_direct = 8.0 * (double)n * (double)m * 0.5;
@@ -451,7 +550,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
                     std::to_string(maxP) + "; got N=" + std::to_string(n) + ", alpha=" + std::to_string(a) + "/" +
                     std::to_string(d) + "; use the naive transform for this pair");
   } else if (method == ASX_CHIRP && !chirp_ok) {
-    return fail(ASX_ERR_UNSUPPORTED, "chirp path needs N+M-1 <= " + std::to_string(maxP) + " for this dtype");
+    return fail(ASX_ERR_UNSUPPORTED, "chirp path needs N+M-1 <= " + std::to_string(maxP * 1024) + " for this dtype");
   }
   if (chosen == ASX_DIRECT && (n * m > (int64_t(1) << 31)))
     return fail(ASX_ERR_UNSUPPORTED, "direct W matrix beyond 2^31 entries; use method fft/chirp");
@@ -513,6 +612,17 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     chirp_sz = std::max(n, m);
     H_sz = p->P;
   }
+  int64_t twP1_sz = 0, twBig_sz = 0, A_sz = 0;
+  if (chosen == ASX_CHIRP && chirp_large) {
+    p->large = 1;
+    p->P2 = maxP;
+    p->P1 = chirp_P / maxP;
+    twP_sz = two_level_size(p->P2, lf_of_P((int)p->P2));  // row FFT table W_P2
+    twP1_sz = two_level_size(p->P1, lf_of_P((int)p->P1));
+    p->lfBig = two_level_lf(chirp_P);
+    twBig_sz = two_level_size(chirp_P, p->lfBig);
+    A_sz = chirp_P;  // four-step workspace
+  }
   if (chosen == ASX_DIRECT) W_sz = m * n;
   p->tw_elems = (int)twA_sz;  // shared-memory table: α pre-twiddle only
   auto align = [](size_t v) { return (v + 31) & ~size_t(31); };
@@ -526,6 +636,12 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   elems += align(H_sz);
   p->off_W = elems * es;
   elems += align(W_sz);
+  p->off_twP1 = elems * es;
+  elems += align(twP1_sz);
+  p->off_twBig = elems * es;
+  elems += align(twBig_sz);
+  p->off_A = elems * es;
+  elems += align(A_sz);
   p->table_bytes = std::max<size_t>(elems * es, 64);
 
   cudaError_t e = cudaMalloc(&p->tables, p->table_bytes);
@@ -541,15 +657,43 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     return cuda_fail(e, "cudaStreamCreate");
   }
   char* base = static_cast<char*>(p->tables);
-  if (twP_sz) fill_two_level(base + p->off_twP, p->P, lf_of_P(p->P), dbl, st);
+  if (twP_sz) fill_two_level(base + p->off_twP, p->large ? p->P2 : p->P, lf_of_P(p->large ? (int)p->P2 : p->P), dbl, st);
+  if (twP1_sz) fill_two_level(base + p->off_twP1, p->P1, lf_of_P((int)p->P1), dbl, st);
+  if (twBig_sz) fill_two_level(base + p->off_twBig, chirp_P, p->lfBig, dbl, st);
   if (twA_sz) fill_two_level(base + p->off_twA, p->r * p->P, p->lfA, dbl, st);
   double2* wP_d = nullptr;
   if (chosen == ASX_CHIRP) {
     const uint64_t L2 = 2ull * (uint64_t)d * (uint64_t)n;
     k_fill_chirp<<<(unsigned)std::min<int64_t>((chirp_sz + 255) / 256, 4096), 256, 0, st>>>(
         base + p->off_chirp, chirp_sz, (uint64_t)a, L2, dbl);
-    e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), sizeof(double2) * p->P, st);
-    if (e == cudaSuccess) {
+    if (p->large) {
+      // H = FFT(h)/P with the same four-step kernels: h -> A (columns), rows -> Ht
+      void* hbuf = nullptr;
+      e = cudaMallocAsync(&hbuf, es * chirp_P, st);
+      if (e == cudaSuccess) {
+        if (dbl)
+          k_fill_h<double><<<4096, 256, 0, st>>>(hbuf, base + p->off_chirp, chirp_P, n, m);
+        else
+          k_fill_h<float><<<4096, 256, 0, st>>>(hbuf, base + p->off_chirp, chirp_P, n, m);
+        LParams lp;
+        std::memset(&lp, 0, sizeof(lp));
+        lp.n = n;
+        lp.m = m;
+        lp.h = hbuf;
+        lp.A = base + p->off_A;
+        lp.Hout = base + p->off_H;
+        lp.twP1 = base + p->off_twP1;
+        lp.twP2 = base + p->off_twP;
+        lp.twBig = base + p->off_twBig;
+        lp.lfBig = p->lfBig;
+        lp.scale = 1.0 / (double)chirp_P;
+        lp.P = chirp_P;
+        lp.P2 = p->P2;
+        e = launch_large(dbl, p->P1, COL_FWD_TABLE, 0, 0, lp, st);
+        if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_SPECTRUM, 1, lp, st);
+        cudaFreeAsync(hbuf, st);
+      }
+    } else if ((e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), sizeof(double2) * p->P, st)) == cudaSuccess) {
       k_fill_roots<<<(p->P + 255) / 256, 256, 0, st>>>(wP_d, p->P, 1, (uint64_t)p->P, 1);
       k_chirp_spectrum<<<(p->P + 127) / 128, 128, 0, st>>>(base + p->off_H, p->P, n, m, (uint64_t)a, L2, wP_d,
                                                            dbl);
@@ -606,7 +750,7 @@ int asx_plan_query(asx_plan_t p, asx_plan_info* info) {
   info->predicted_mults = p->pred_mults;
   info->predicted_adds = p->pred_adds;
   info->workspace_bytes = (int64_t)p->table_bytes;
-  info->kernels_per_execute = 1;
+  info->kernels_per_execute = p->large ? 3 : 1;
   info->device = p->device;
   return ASX_OK;
 }

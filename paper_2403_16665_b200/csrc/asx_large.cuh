@@ -1,0 +1,194 @@
+// asx_large.cuh — chirp-z α-DFT for signals whose cyclic FFT size P exceeds
+// one CTA (BASELINE config 2: N = 2^22, α = 1/16, P = 2^23), as a four-step
+// FFT P = P1 x P2 through an HBM/L2 workspace.
+//
+// Index maps (n = P2*n1 + n2, k = k1 + P1*k2 for the forward transform; the
+// inverse reuses the transposed map k = k1 + P1*k2 -> n = c + P2*d):
+//   KA  k_large_cols<FWD>: per tile of 8 columns n2, FFT_P1 over n1 of
+//       y[P2 n1 + n2] (y = x*chirp, zero past N), times W_P^{n2 k1}
+//       -> A[k1][n2]                                  (coalesced 8-wide rows)
+//   KB  k_large_rows<MAIN>: per row k1, FFT_P2 over n2 -> Y[k1 + P1 k2],
+//       times Ht[k1][k2] = H[k1 + P1 k2]/P, conj, FFT_P2 over k2, times
+//       W_P^{k1 c} -> B[k1][c]       (forward step 3 + inverse step 1 fused:
+//       the spectrum never leaves the CTA)
+//   KC  k_large_cols<INV>: per tile of 8 columns c, FFT_P1 over k1 of
+//       B[k1][c] -> G[c + P2 d]; X[m] = chirp[m] * conj(G[m]) for m < M.
+// The plan builds Ht with KA (on h) + k_large_rows<SPECTRUM>.
+#pragma once
+
+#include "asx_kernels.cuh"
+
+namespace asx {
+
+constexpr int kColTile = 8;  // columns per CTA in the column kernels (8 x 16 B = 128 B rows)
+
+struct LParams {
+  const void* x;  // input row (real or complex), N samples
+  int real_in;
+  int64_t n, m;
+  void* X;              // output row, M bins
+  const void* chirp;    // chirp[k], k < max(N, M)
+  const void* h;        // KA on the kernel table (plan time): complex h[P]
+  void* A;              // workspace P complex (row-major [P1][P2])
+  const void* Ht;       // spectrum table [P1][P2]
+  void* Hout;           // plan time: spectrum output
+  const void* twP1;     // two-level W_P1
+  const void* twP2;     // two-level W_P2
+  const void* twBig;    // two-level W_P
+  int lfBig;
+  double scale;         // plan time: 1/P
+  int64_t P;            // P1 * P2
+  int64_t P2;           // row length (row stride of A / Ht)
+};
+
+template <typename C>
+__device__ __forceinline__ C tw_big(const C* tw, uint64_t k, int lf) {
+  const C f = __ldg(tw + (k & ((uint64_t(1) << lf) - 1)));
+  const C c = __ldg(tw + (uint64_t(1) << lf) + (k >> lf));
+  return cmul(f, c);
+}
+
+enum { COL_FWD_SIGNAL = 0, COL_FWD_TABLE = 1, COL_INV_OUT = 2 };
+
+template <typename Real, int P1>
+struct ColCfg {
+  static constexpr int R = P1 < 8 ? P1 : 8;
+  static constexpr int NT = P1 / R;
+  using E = Fft<Real, P1, NT>;
+  static constexpr size_t SMEM = size_t(kColTile) * (P1 + (P1 >> E::LPAD)) * sizeof(typename CT<Real>::T);
+};
+
+// 8 teams of NT threads, one column each; the tile passes through the teams'
+// shared buffers on the way in and out so HBM sees 128 B row segments.
+template <typename Real, int P1, int NT, int MODE>
+__global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
+  using E = Fft<Real, P1, NT>;
+  using C = typename CT<Real>::T;
+  constexpr int R = E::R;
+  constexpr int THREADS = NT * kColTile;
+  const int64_t P2 = p.P2;
+  const uint64_t Pmask = uint64_t(p.P - 1);
+  constexpr int CS = P1 + (P1 >> E::LPAD);  // per-column tile stride (>= SMEM_ELEMS)
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* smbase = reinterpret_cast<C*>(smraw);
+  const int team = threadIdx.x / NT, t = threadIdx.x % NT;
+  C* sm = smbase + team * CS;
+  const int col0 = blockIdx.x * kColTile;
+  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP1));
+
+  // ---- gather the 8-column tile: 8 threads per row, rows strided ----
+  {
+    const int tau = threadIdx.x & (kColTile - 1);
+    for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
+      const int64_t idx = int64_t(row) * P2 + col0 + tau;  // element index
+      C val = mk(Real(0), Real(0));
+      if constexpr (MODE == COL_FWD_SIGNAL) {
+        if (idx < p.n) {  // y[n] = x[n] * chirp[n], zero past N
+          const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(p.x) + idx), Real(0))
+                                 : __ldg(reinterpret_cast<const C*>(p.x) + idx);
+          val = cmul(xv, __ldg(reinterpret_cast<const C*>(p.chirp) + idx));
+        }
+      } else if constexpr (MODE == COL_FWD_TABLE) {
+        val = __ldg(reinterpret_cast<const C*>(p.h) + idx);
+      } else {
+        val = __ldg(reinterpret_cast<const C*>(p.A) + idx);  // B[k1][c], row = k1
+      }
+      smbase[tau * CS + E::pad(row)] = val;
+    }
+  }
+  __syncthreads();
+  C v[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = sm[E::pad(t + NT * i)];
+  E::run(v, sm, t, tr);  // starts with a barrier before reusing sm
+  const int col = col0 + team;
+  if constexpr (MODE != COL_INV_OUT) {
+    // twiddle W_P^{n2 k1}, k1 = t + NT*i
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t k1 = uint64_t(t + NT * i);
+      v[i] = cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (k1 * uint64_t(col)) & Pmask, p.lfBig));
+      if ((i & 3) == 3) reg_fence();
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
+  __syncthreads();
+  {
+    const int tau = threadIdx.x & (kColTile - 1);
+    for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
+      const C val = smbase[tau * CS + E::pad(row)];
+      if constexpr (MODE != COL_INV_OUT) {
+        reinterpret_cast<C*>(p.A)[int64_t(row) * P2 + col0 + tau] = val;
+      } else {
+        const int64_t mm = int64_t(col0 + tau) + P2 * row;  // m = c + P2 d
+        if (mm < p.m)
+          reinterpret_cast<C*>(p.X)[mm] = cmul(cconj(val), __ldg(reinterpret_cast<const C*>(p.chirp) + mm));
+      }
+    }
+  }
+}
+
+enum { ROW_SPECTRUM = 0, ROW_MAIN = 1 };
+
+template <typename Real, int P2, int NT, int MODE>
+__global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
+  using E = Fft<Real, P2, NT>;
+  using C = typename CT<Real>::T;
+  constexpr int R = E::R;
+  const uint64_t Pmask = uint64_t(p.P - 1);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* sm = reinterpret_cast<C*>(smraw);
+  const int t = threadIdx.x;
+  const int k1 = blockIdx.x;
+  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP2));
+  C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * P2;
+  C v[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = row[t + NT * i];
+  if constexpr (MODE == ROW_SPECTRUM) {
+    E::run(v, sm, t, tr);
+    C* out = reinterpret_cast<C*>(p.Hout) + int64_t(k1) * P2;
+    const Real s = Real(p.scale);
+#pragma unroll
+    for (int i = 0; i < R; ++i) out[t + NT * i] = mk(v[i].x * s, v[i].y * s);
+  } else {
+    const C* ht = reinterpret_cast<const C*>(p.Ht) + int64_t(k1) * P2;
+    // one FFT body, two trips (forward step 3, then inverse step 1)
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      E::run(v, sm, t, tr);
+      if (half == 0) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          v[i] = cconj(cmul(v[i], __ldg(ht + t + NT * i)));
+          if ((i & 3) == 3) reg_fence();
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t c = uint64_t(t + NT * i);
+      row[t + NT * i] =
+          cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(k1) * c) & Pmask, p.lfBig));
+      if ((i & 3) == 3) reg_fence();
+    }
+  }
+}
+
+// h[j] = conj(chirp[j]) (j < M), conj(chirp[P-j]) (P-j < N), else 0.
+template <typename Real>
+__global__ void k_fill_h(void* h, const void* chirp, int64_t P, int64_t n, int64_t m) {
+  using C = typename CT<Real>::T;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < P; j += int64_t(gridDim.x) * blockDim.x) {
+    C v = mk(Real(0), Real(0));
+    if (j < m)
+      v = cconj(__ldg(reinterpret_cast<const C*>(chirp) + j));
+    else if (P - j < n)
+      v = cconj(__ldg(reinterpret_cast<const C*>(chirp) + (P - j)));
+    reinterpret_cast<C*>(h)[j] = v;
+  }
+}
+
+}  // namespace asx

@@ -290,3 +290,48 @@ def test_linearity_at_scale(asx, torch):
         rhs = p.execute(x) + 2 * p.execute(y)
         scale = lhs.abs().amax(dim=1)
         assert float(((lhs - rhs).abs().amax(dim=1) / scale).max()) <= TOL32
+
+
+# ------------------------------------------------- four-step (large P) path
+
+@pytest.mark.parametrize("n,a,d,m,dtype", [
+    (8192, 1, 8, 8192, "complex128"),    # P = 16384 = 2 x 8192
+    (6000, 3, 7, 5000, "complex128"),    # non-power-of-two N, non-dyadic alpha
+    (16384, 1, 2, 16384, "complex64"),   # P = 32768 = 2 x 16384
+    (1 << 18, 1, 16, 1 << 18, "complex64"),  # P = 2^19 = 32 x 16384
+])
+def test_large_chirp_vs_oracle(asx, n, a, d, m, dtype):
+    rng = np.random.default_rng(n + d)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(2)])
+    if dtype == "complex64":
+        x = x.astype(np.complex64)
+    got, p = gpu_run(asx, x, a, d, m, "chirp", dtype=dtype)
+    assert p.info.kernels_per_execute == 3 and p.fft_size > (8192 if dtype == "complex128" else 16384)
+    if n * m <= (1 << 26):
+        want = orc.direct(x.astype(np.complex128), a, d, m)
+    else:  # zero-padded FFT == first M bins of the density-d spectrum (alpha = 1/d)
+        assert a == 1
+        want = np.fft.fft(x.astype(np.complex128), d * n, axis=1)[:, :m]
+    tol = TOL64 if dtype == "complex128" else TOL32
+    assert orc.rel_err(got, want) <= tol
+
+
+def test_config2_full_size(asx):
+    """BASELINE config 2: N = 2^22 real f64, alpha = 1/16, M = N (four-step chirp)."""
+    from paper_2403_16665_b200.signals import WORKLOADS, generate
+
+    w = WORKLOADS["2"]
+    x = generate(w, 0, 1)[0]
+    got, p = gpu_run(asx, x[None], 1, 16, w.m, "auto", real=True)
+    assert p.method == "chirp"
+    # independent check: zero-padded FFT (pocketfft) of length 16N, first N bins
+    want = np.fft.fft(x, 16 * w.n)[: w.m]
+    assert orc.rel_err(got, want[None]) <= TOL64
+    # exact-reduction direct sums on sampled bins (ref/oracle.py:37-47 semantics)
+    bins = np.array([0, 1, 7, 12345, w.m // 2, w.m - 1])
+    nn = np.arange(w.n, dtype=np.int64)
+    L = 16 * w.n
+    for b in bins:
+        idx = (b * nn) % L
+        want_b = np.sum(x * np.exp(-2j * np.pi * idx / L))
+        assert abs(got[0, b] - want_b) <= TOL64 * np.max(np.abs(got))
