@@ -47,19 +47,9 @@ def parse_args():
     return ap.parse_args()
 
 
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    return world, rank, local
-
-
-def shard_range(total: int, world: int, rank: int):
-    """Contiguous shard [lo, hi) of a batch of `total` signals."""
-    base, extra = divmod(total, world)
-    lo = rank * base + min(rank, extra)
-    hi = lo + base + (1 if rank < extra else 0)
-    return lo, hi
+from paper_2403_16665_b200.dist import barrier as dist_barrier  # noqa: E402
+from paper_2403_16665_b200.dist import gather_checksums, max_over_ranks, shard_range  # noqa: E402
+from paper_2403_16665_b200.dist import world as dist_env  # noqa: E402
 
 
 def measured_peaks():
@@ -202,9 +192,7 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    barrier = dist_barrier
 
     w = WORKLOADS[args.config]
     total = args.batch or w.batch
@@ -239,10 +227,7 @@ def run_gpu(args):
     barrier()
     step_ms = [s.elapsed_time(e) for s, e in evs]
     tot_ms = sum(step_ms)
-    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    tot_ms_max = float(t.item())
+    tot_ms_max = max_over_ranks(tot_ms, device=dev)
     ms_per_step = tot_ms_max / args.steps
     value = total * w.m / (ms_per_step / 1e3)
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / avg launch duration
@@ -265,10 +250,7 @@ def run_gpu(args):
             plan.execute_host(hxn, out=hXn)
         el = time.perf_counter() - t0
         barrier()
-        tt = torch.tensor([el], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item()) / args.e2e_steps
+        e2e_s = max_over_ranks(el, device=dev) / args.e2e_steps
         elem_in = x.element_size()
         e2e = {"value": total * w.m / e2e_s, "unit": "complex points/s",
                "h2d_bytes_per_step": nloc * w.n * elem_in, "d2h_bytes_per_step": nloc * w.m * out.element_size(),
@@ -278,14 +260,7 @@ def run_gpu(args):
         e2e["matches_device_path"] = bool(same)
 
     # untimed verification collective: per-rank checksums gathered over NCCL
-    chk = torch.tensor([float(out.abs().amax().item()), float(out.real.sum().item())], dtype=torch.float64,
-                       device=dev)
-    if world > 1:
-        gathered = [torch.zeros_like(chk) for _ in range(world)]
-        dist.all_gather(gathered, chk)
-        checks = [g.tolist() for g in gathered]
-    else:
-        checks = [chk.tolist()]
+    checks = gather_checksums(out, device=dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
