@@ -134,7 +134,8 @@ int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype
                   void* stream);
 
 /* Launch shape of the last FFT-family kernel this thread launched: grid,
- * block, dynamic shared memory and whether rows were TMA-staged. */
+ * block, dynamic shared memory; *staged bit 0 = rows TMA-staged, bit 1 =
+ * chirp tables held in tensor memory. */
 int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged);
 
 const char* asx_strerror(int status);

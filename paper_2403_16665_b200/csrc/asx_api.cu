@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -68,12 +69,13 @@ constexpr int kMaxP_c128 = 8192;
 struct LaunchEnv {
   int sms = 148;
   size_t smem_optin = 227 * 1024;
+  int use_tmem = 1;  // chirp tables in tensor memory (env ASX_NO_TMEM=1 disables, for A/B runs)
 };
 
 // Shape of the most recent launch on this thread (asx_last_launch, for
 // benchmarks / tests that report occupancy decisions).
 struct LastLaunch {
-  int grid = 0, block = 0, smem = 0, staged = 0;
+  int grid = 0, block = 0, smem = 0, staged = 0, tmem = 0;
 };
 thread_local LastLaunch g_last_launch;
 
@@ -210,7 +212,24 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
   const int64_t need = (batch + G::TPB - 1) / G::TPB;
   const int64_t grid = std::min<int64_t>(need, int64_t(env.sms) * per_sm);
   kp.batch = batch;
-  kern<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
+  int tm_used = 0;
+  if constexpr (KIND == KIND_CHIRP && G::TPB == 1 && TmemCfg<Real, G::NT, G::R>::OK) {
+    using TMC = TmemCfg<Real, G::NT, G::R>;
+    if (env.use_tmem && per_sm * TMC::NCOLS <= 512) {
+      auto kern_tm = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, true>;
+      static thread_local int tm_attr_for = -1;
+      if (tm_attr_for != dev) {
+        cudaError_t e = cudaFuncSetAttribute(kern_tm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)env.smem_optin);
+        if (e != cudaSuccess) return e;
+        tm_attr_for = dev;
+      }
+      kern_tm<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
+      tm_used = 1;
+    }
+  }
+  if (!tm_used) kern<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
+  g_last_launch.tmem = tm_used;
   g_last_launch.grid = (int)grid;
   g_last_launch.block = G::NT * G::TPB;
   g_last_launch.smem = (int)smem;
@@ -297,7 +316,7 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
   constexpr int P2 = sizeof(Real) == 4 ? 16384 : 8192;
   using G = Cfg<P2, Real>;
   using E = Fft<Real, P2, G::NT>;
-  const size_t smem = size_t(E::SMEM_ELEMS) * sizeof(typename CT<Real>::T);
+  const size_t smem = size_t(E::SMEM_ELEMS + E::TAB_ELEMS) * sizeof(typename CT<Real>::T);
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kern) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -371,11 +390,13 @@ void fill_kparams(const asx_plan_s* p, KParams& kp) {
   kp.H = base + p->off_H;
   kp.W = base + p->off_W;
   kp.tw_elems = p->tw_elems;
+  kp.chirp_len = std::max(p->n, p->m);
 }
 
 int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs, int64_t batch,
                    cudaStream_t st) {
   if (batch == 0 || p->m == 0) return ASX_OK;
+  if (batch > 0x7fffffffLL) return fail(ASX_ERR_INVALID, "batch must be < 2^31 per call");
   KParams kp;
   fill_kparams(p, kp);
   kp.x = x;
@@ -474,7 +495,7 @@ int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged) {
   if (grid) *grid = g_last_launch.grid;
   if (block) *block = g_last_launch.block;
   if (smem_bytes) *smem_bytes = g_last_launch.smem;
-  if (staged) *staged = g_last_launch.staged;
+  if (staged) *staged = g_last_launch.staged | (g_last_launch.tmem << 1);
   return ASX_OK;
 }
 
@@ -519,7 +540,9 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     fft_fold = a;
     fft_P = n / a;
   }
-  const int64_t chirp_P = next_pow2(n + m - 1);
+  // P >= N + M - 1 (linear convolution) and P >= 2N (the chirp kernel treats
+  // the upper half of its FFT input as compile-time zero padding)
+  const int64_t chirp_P = next_pow2(std::max(n + m - 1, 2 * n));
   // one CTA per transform up to maxP; beyond, the four-step path P = P1 x maxP
   const bool chirp_large = chirp_P > maxP && chirp_P / maxP <= 1024;
   const bool chirp_ok = chirp_P <= maxP || chirp_large;
@@ -579,6 +602,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     return fail(ASX_ERR_CUDA, "cannot select CUDA device " + std::to_string(device) + " (no GPU?)");
   }
   {
+    const char* no_tm = std::getenv("ASX_NO_TMEM");
+    p->env.use_tmem = (no_tm && no_tm[0] == '1') ? 0 : 1;
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) p->env.sms = v;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)

@@ -13,6 +13,13 @@
 
 #include "asx_engine.cuh"
 
+#ifndef ASX_ZERO_PRUNE
+#define ASX_ZERO_PRUNE 1  // chirp: compile-time zero upper half of the FFT input
+#endif
+#ifndef ASX_FENCE_CHUNK
+#define ASX_FENCE_CHUNK 4  // table loads issued per group between compiler fences
+#endif
+
 namespace asx {
 
 struct KParams {
@@ -33,6 +40,7 @@ struct KParams {
   const void* W;       // direct: M x N
   int staged;          // 1: rows fetched by TMA into shared memory
   int tw_elems;        // shared twiddle elements (W_P two-level [+ W_rN two-level])
+  int64_t chirp_len;   // entries of the chirp table (max(N, M))
 };
 
 template <typename C>
@@ -70,11 +78,16 @@ struct PersistLayout {
   __host__ __device__ static size_t stage_bytes(size_t row_bytes, bool staged) {
     return staged ? align_up(row_bytes, 128) : 0;
   }
-  __host__ __device__ static size_t tw_off(size_t row_bytes, bool staged) {
+  static constexpr size_t TAB_BYTES = align_up(size_t(E::TAB_ELEMS) * sizeof(C), 16);
+  __host__ __device__ static size_t tab_off(size_t row_bytes, bool staged) {
     return FFT_BYTES + size_t(TPB) * stage_bytes(row_bytes, staged);
   }
+  __host__ __device__ static size_t tw_off(size_t row_bytes, bool staged) {
+    return tab_off(row_bytes, staged) + TAB_BYTES;
+  }
+  // [fft buffers | stage rows | twiddle tables | α table | mbarriers | TMEM slot]
   __host__ __device__ static size_t total(size_t row_bytes, bool staged, size_t tw_elems) {
-    return align_up(tw_off(row_bytes, staged) + tw_elems * sizeof(C), 16) + TPB * sizeof(uint64_t);
+    return align_up(tw_off(row_bytes, staged) + tw_elems * sizeof(C), 16) + TPB * sizeof(uint64_t) + 16;
   }
 };
 
@@ -105,7 +118,20 @@ struct PersistLayout {
 // ---------------------------------------------------------------------------
 enum { KIND_AFFT = 0, KIND_CHIRP = 1 };
 
-template <typename Real, int P, int NT, int TPB, int KIND, int MINB>
+// TMEM layout of the chirp tables (TM variant, TPB == 1, NT % 128 == 0): warp
+// w owns lanes 32*(w%4).., column slot w/4 of CPT columns: H[t + NT*j] for
+// j < R, then chirp[t + NT*j] for j < R.
+template <typename Real, int NT, int R>
+struct TmemCfg {
+  static constexpr int WPC = sizeof(typename CT<Real>::T) / 4;  // 32-bit words per complex
+  static constexpr int CPT = 2 * R * WPC;                       // columns per thread
+  static constexpr int CPC = 8 / WPC;                           // complex per 8-column access
+  static constexpr int NEED = (NT / 128) * CPT;
+  static constexpr int NCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr bool OK = (NT % 128 == 0) && NEED <= 512;
+};
+
+template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   using E = Fft<Real, P, NT>;
   using L = PersistLayout<Real, P, NT, TPB>;
@@ -122,51 +148,106 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
                       smraw + align_up(L::tw_off(row_bytes, staged) + p.tw_elems * sizeof(C), 16)) + team;
 
   // per-thread pass twiddles -> registers; α pre-twiddle table -> shared
-  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP));
+  const typename E::TwRegs tr =
+      E::make_tw(t, reinterpret_cast<const C*>(p.twP), reinterpret_cast<C*>(smraw + L::tab_off(row_bytes, staged)),
+                 threadIdx.x, NT * TPB);
   {
     const C* srca = reinterpret_cast<const C*>(p.twA);
     for (int i = threadIdx.x; i < p.tw_elems; i += NT * TPB) twa[i] = __ldg(srca + i);
   }
-  const int64_t stride = int64_t(gridDim.x) * TPB;
-  int64_t u = int64_t(blockIdx.x) * TPB + team;
-  const int64_t iters = (p.batch + stride - 1) / stride;
+  // batch < 2^31 (checked on the host): 32-bit signal indices keep the
+  // persistent loop's live state small next to the 2R data registers
+  const int stride = int(gridDim.x) * TPB;
+  int u = int(blockIdx.x) * TPB + team;
+  const int batch = int(p.batch);
+  const int iters = (batch + stride - 1) / stride;
   if (staged && t == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (staged && t == 0 && u < p.batch) {
+  if (staged && t == 0 && u < batch) {
     mbar_expect_tx(bar, (uint32_t)row_bytes);
-    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + u * p.xs * (row_bytes / p.n), (uint32_t)row_bytes,
-                bar);
+    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * (row_bytes / p.n),
+                (uint32_t)row_bytes, bar);
   }
   uint32_t phase = 0;
   const C* chirp = reinterpret_cast<const C*>(p.chirp);
   const C* H = reinterpret_cast<const C*>(p.H);
+  using TMC = TmemCfg<Real, NT, R>;
+  uint32_t tbase = 0;
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar - team + TPB);  // after the mbarriers
+  if constexpr (TM) {
+    static_assert(TPB == 1 && TMC::OK, "TMEM tables need one team per CTA");
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tmem_alloc(&tmem_slot, TMC::NCOLS);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * TMC::CPT);
+#pragma unroll
+    for (int j0 = 0; j0 < R; j0 += TMC::CPC) {
+      uint32_t wh[8], wc[8];
+#pragma unroll
+      for (int k = 0; k < TMC::CPC; ++k) {
+        const int idx = t + NT * (j0 + k);
+        c_to_words(__ldg(H + idx), &wh[k * TMC::WPC]);
+        c_to_words(idx < p.chirp_len ? __ldg(chirp + idx) : mk(Real(0), Real(0)), &wc[k * TMC::WPC]);
+      }
+      tmem_st8(tbase + j0 * TMC::WPC, wh);
+      tmem_st8(tbase + (R + j0) * TMC::WPC, wc);
+    }
+    tmem_wait_st();
+  }
+  // chirp / kernel-spectrum value j of this thread (TMEM or L2)
+  auto tab_chunk = [&](int which, int j0, C (&out)[TMC::CPC]) {
+    if constexpr (TM) {
+      uint32_t w[8];
+      tmem_ld8(tbase + (which * R + j0) * TMC::WPC, w);
+#pragma unroll
+      for (int k = 0; k < TMC::CPC; ++k) out[k] = words_to_c(&w[k * TMC::WPC], (C*)nullptr);
+    } else {
+#pragma unroll
+      for (int k = 0; k < TMC::CPC; ++k) {
+        const int idx = t + NT * (j0 + k);
+        out[k] = mk(Real(0), Real(0));
+        if (j0 + k < R)
+          out[k] = which == 0 ? __ldg(H + idx) : (idx < p.chirp_len ? __ldg(chirp + idx) : mk(Real(0), Real(0)));
+      }
+    }
+  };
 
-  for (int64_t it = 0; it < iters; ++it, u += stride) {
-    const bool live = u < p.batch;
-    const int64_t row_off = u * p.xs;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it, u += stride) {
+    const bool live = u < batch;
+    const int64_t row_off = int64_t(u) * p.xs;
     if constexpr (KIND == KIND_CHIRP) {
       C v[R];
       if (staged && live) {
         mbar_wait(bar, phase);
         phase ^= 1;
       }
+      // the plan guarantees P >= 2N: elements t + NT*i with i >= R/2 are the
+      // zero padding, known at compile time (first pass folds them away)
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int nn = t + NT * i;
-        C val = mk(Real(0), Real(0));
-        if (live && nn < p.n) val = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), __ldg(chirp + nn));
-        v[i] = val;
-        if ((i & 3) == 3) reg_fence();
+      for (int i = 0; i < R; ++i) v[i] = mk(Real(0), Real(0));
+      constexpr int RIN = (ASX_ZERO_PRUNE && R > 1) ? R / 2 : R;
+#pragma unroll
+      for (int j0 = 0; j0 < RIN; j0 += (TMC::CPC < RIN ? TMC::CPC : RIN)) {
+        C cw[TMC::CPC];
+        tab_chunk(1, j0, cw);
+#pragma unroll
+        for (int k = 0; k < TMC::CPC && j0 + k < RIN; ++k) {
+          const int nn = t + NT * (j0 + k);
+          if (live && nn < p.n) v[j0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+        }
       }
       if (staged) {
         __syncthreads();  // the whole row has been consumed
-        if (t == 0 && u + stride < p.batch) {
+        if (t == 0 && u + stride < batch) {
           fence_proxy_async();
           mbar_expect_tx(bar, (uint32_t)row_bytes);
-          tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + (u + stride) * p.xs * (row_bytes / p.n),
+          tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * (row_bytes / p.n),
                       (uint32_t)row_bytes, bar);
         }
       }
@@ -177,19 +258,25 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         E::run(v, fbuf, t, tr);
         if (half == 0) {
 #pragma unroll
-          for (int i = 0; i < R; ++i) {
-            v[i] = cconj(cmul(v[i], __ldg(H + t + NT * i)));
-            if ((i & 3) == 3) reg_fence();
+          for (int j0 = 0; j0 < R; j0 += TMC::CPC) {
+            C hw[TMC::CPC];
+            tab_chunk(0, j0, hw);
+#pragma unroll
+            for (int k = 0; k < TMC::CPC && j0 + k < R; ++k) v[j0 + k] = cconj(cmul(v[j0 + k], hw[k]));
           }
         }
       }
       if (live) {
-        C* X = reinterpret_cast<C*>(p.X) + u * p.Xs;
+        C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const int mm = t + NT * i;
-          if (mm < p.m) X[mm] = cmul(cconj(v[i]), __ldg(chirp + mm));
-          if ((i & 3) == 3) reg_fence();
+        for (int j0 = 0; j0 < R; j0 += TMC::CPC) {
+          C cw[TMC::CPC];
+          tab_chunk(1, j0, cw);
+#pragma unroll
+          for (int k = 0; k < TMC::CPC && j0 + k < R; ++k) {
+            const int mm = t + NT * (j0 + k);
+            if (mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+          }
         }
       }
     } else {
@@ -223,16 +310,17 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         }
         if (staged && c == p.r - 1) {
           __syncthreads();
-          if (t == 0 && u + stride < p.batch) {
+          if (t == 0 && u + stride < batch) {
             fence_proxy_async();
             mbar_expect_tx(bar, (uint32_t)row_bytes);
-            tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + (u + stride) * p.xs * (row_bytes / p.n),
+            tma_load_1d(stage,
+                        static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * (row_bytes / p.n),
                         (uint32_t)row_bytes, bar);
           }
         }
         E::run(v, fbuf, t, tr);
         if (live) {
-          C* X = reinterpret_cast<C*>(p.X) + u * p.Xs;
+          C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
           const int64_t period = p.r * P;
 #pragma unroll
           for (int i = 0; i < R; ++i) {
@@ -242,6 +330,12 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         }
       }
     }
+  }
+  if constexpr (TM) {
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if ((threadIdx.x >> 5) == 0) tmem_dealloc(tmem_slot, TMC::NCOLS);
   }
 }
 

@@ -55,7 +55,8 @@ struct ColCfg {
   static constexpr int R = P1 < 8 ? P1 : 8;
   static constexpr int NT = P1 / R;
   using E = Fft<Real, P1, NT>;
-  static constexpr size_t SMEM = size_t(kColTile) * (P1 + (P1 >> E::LPAD)) * sizeof(typename CT<Real>::T);
+  static constexpr size_t SMEM =
+      (size_t(kColTile) * (P1 + (P1 >> E::LPAD)) + E::TAB_ELEMS) * sizeof(typename CT<Real>::T);
 };
 
 // 8 teams of NT threads, one column each; the tile passes through the teams'
@@ -74,7 +75,8 @@ __global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
   const int team = threadIdx.x / NT, t = threadIdx.x % NT;
   C* sm = smbase + team * CS;
   const int col0 = blockIdx.x * kColTile;
-  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP1));
+  C* tabp = smbase + kColTile * CS;
+  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP1), tabp, threadIdx.x, THREADS);
 
   // ---- gather the 8-column tile: 8 threads per row, rows strided ----
   {
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
     for (int i = 0; i < R; ++i) {
       const uint64_t k1 = uint64_t(t + NT * i);
       v[i] = cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (k1 * uint64_t(col)) & Pmask, p.lfBig));
-      if ((i & 3) == 3) reg_fence();
+      if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
     }
   }
   __syncthreads();
@@ -142,7 +144,9 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
   C* sm = reinterpret_cast<C*>(smraw);
   const int t = threadIdx.x;
   const int k1 = blockIdx.x;
-  const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP2));
+  const typename E::TwRegs tr =
+      E::make_tw(t, reinterpret_cast<const C*>(p.twP2), sm + E::SMEM_ELEMS, threadIdx.x, NT);
+  __syncthreads();
   C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * P2;
   C v[R];
 #pragma unroll
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           v[i] = cconj(cmul(v[i], __ldg(ht + t + NT * i)));
-          if ((i & 3) == 3) reg_fence();
+          if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
         }
       }
     }
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
       const uint64_t c = uint64_t(t + NT * i);
       row[t + NT * i] =
           cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(k1) * c) & Pmask, p.lfBig));
-      if ((i & 3) == 3) reg_fence();
+      if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
     }
   }
 }

@@ -209,9 +209,11 @@ def test_random_vs_oracle(asx, n, a, d, m, methods, dtype):
         assert err <= tol, (method, err)
 
 
-def test_oversize_chirp_is_refused(asx):
+def test_oversize_chirp_goes_four_step(asx):
+    p = asx.plan(8192, asx.DenseFactor(8), m=8192, method="chirp", dtype="complex128")
+    assert p.info.kernels_per_execute == 3 and p.fft_size == 16384
     with pytest.raises(asx.UnsupportedSizeError):
-        asx.plan(8192, asx.DenseFactor(8), m=8192, method="chirp", dtype="complex128")
+        asx.plan(1 << 23, asx.DenseFactor(8), m=1 << 23, method="chirp", dtype="complex128")
 
 
 def test_alpha_fft_matches_reference_recursion_output(asx):
