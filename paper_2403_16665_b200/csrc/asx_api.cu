@@ -316,7 +316,7 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
   constexpr int P2 = sizeof(Real) == 4 ? 16384 : 8192;
   using G = Cfg<P2, Real>;
   using E = Fft<Real, P2, G::NT>;
-  const size_t smem = size_t(E::SMEM_ELEMS + E::TAB_ELEMS) * sizeof(typename CT<Real>::T);
+  const size_t smem = size_t(E::SMEM_ELEMS + E::TAB_ELEMS + 2) * sizeof(typename CT<Real>::T) + 16;
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kern) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

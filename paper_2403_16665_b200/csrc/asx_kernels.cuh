@@ -88,6 +88,7 @@ struct PersistLayout {
   // [fft buffers | stage rows | twiddle tables | α table | mbarriers | TMEM slot]
   __host__ __device__ static size_t total(size_t row_bytes, bool staged, size_t tw_elems) {
     return align_up(tw_off(row_bytes, staged) + tw_elems * sizeof(C), 16) + TPB * sizeof(uint64_t) + 16;
+    // tail: TPB TMA mbarriers, the exchange WAR mbarrier, the TMEM address slot
   }
 };
 
@@ -165,6 +166,8 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
+  typename E::XSync xs;
+  E::xs_init(xs, bar - team + TPB, NT * TPB);
   __syncthreads();
   if (staged && t == 0 && u < batch) {
     mbar_expect_tx(bar, (uint32_t)row_bytes);
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   const C* H = reinterpret_cast<const C*>(p.H);
   using TMC = TmemCfg<Real, NT, R>;
   uint32_t tbase = 0;
-  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar - team + TPB);  // after the mbarriers
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar - team + TPB + 1);  // after the mbarriers
   if constexpr (TM) {
     static_assert(TPB == 1 && TMC::OK, "TMEM tables need one team per CTA");
     const int warp = threadIdx.x >> 5;
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
       // a 2-trip loop so only one copy of the transform is register-allocated
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
-        E::run(v, fbuf, t, tr);
+        E::run(v, fbuf, t, tr, xs);
         if (half == 0) {
 #pragma unroll
           for (int j0 = 0; j0 < R; j0 += TMC::CPC) {
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
                         (uint32_t)row_bytes, bar);
           }
         }
-        E::run(v, fbuf, t, tr);
+        E::run(v, fbuf, t, tr, xs);
         if (live) {
           C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
           const int64_t period = p.r * P;

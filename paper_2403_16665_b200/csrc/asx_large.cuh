@@ -56,7 +56,7 @@ struct ColCfg {
   static constexpr int NT = P1 / R;
   using E = Fft<Real, P1, NT>;
   static constexpr size_t SMEM =
-      (size_t(kColTile) * (P1 + (P1 >> E::LPAD)) + E::TAB_ELEMS) * sizeof(typename CT<Real>::T);
+      (size_t(kColTile) * (P1 + (P1 >> E::LPAD)) + E::TAB_ELEMS + 2) * sizeof(typename CT<Real>::T) + 16;
 };
 
 // 8 teams of NT threads, one column each; the tile passes through the teams'
@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
   const int col0 = blockIdx.x * kColTile;
   C* tabp = smbase + kColTile * CS;
   const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP1), tabp, threadIdx.x, THREADS);
+  typename E::XSync xs;
+  E::xs_init(xs, reinterpret_cast<uint64_t*>(tabp + E::TAB_ELEMS + (E::TAB_ELEMS & 1)), THREADS);
 
   // ---- gather the 8-column tile: 8 threads per row, rows strided ----
   {
@@ -102,7 +104,8 @@ __global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
   C v[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) v[i] = sm[E::pad(t + NT * i)];
-  E::run(v, sm, t, tr);  // starts with a barrier before reusing sm
+  __syncthreads();       // tile reads done before the transform reuses sm
+  E::run(v, sm, t, tr, xs);
   const int col = col0 + team;
   if constexpr (MODE != COL_INV_OUT) {
     // twiddle W_P^{n2 k1}, k1 = t + NT*i
@@ -146,13 +149,15 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
   const int k1 = blockIdx.x;
   const typename E::TwRegs tr =
       E::make_tw(t, reinterpret_cast<const C*>(p.twP2), sm + E::SMEM_ELEMS, threadIdx.x, NT);
+  typename E::XSync xs;
+  E::xs_init(xs, reinterpret_cast<uint64_t*>(sm + E::SMEM_ELEMS + E::TAB_ELEMS + (E::TAB_ELEMS & 1)), NT);
   __syncthreads();
   C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * P2;
   C v[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) v[i] = row[t + NT * i];
   if constexpr (MODE == ROW_SPECTRUM) {
-    E::run(v, sm, t, tr);
+    E::run(v, sm, t, tr, xs);
     C* out = reinterpret_cast<C*>(p.Hout) + int64_t(k1) * P2;
     const Real s = Real(p.scale);
 #pragma unroll
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
     // one FFT body, two trips (forward step 3, then inverse step 1)
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {
-      E::run(v, sm, t, tr);
+      E::run(v, sm, t, tr, xs);
       if (half == 0) {
 #pragma unroll
         for (int i = 0; i < R; ++i) {
