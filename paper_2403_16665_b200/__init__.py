@@ -33,6 +33,14 @@ from .transforms import (
     predicted_mults,
     transform_samples,
 )
+from .comparators import (
+    PaddedSignal,
+    aliased_reconstruct,
+    naive_inverse,
+    orthogonality_kernel,
+    standard_fft,
+    zero_pad,
+)
 from ._lib import AsxCudaError, LIB_PATH
 
 __version__ = "0.1.0"
@@ -42,5 +50,6 @@ __all__ = [
     "ValidatedPair", "bin_frequency", "density_for_alpha", "is_power_of_two", "make_dense_factor",
     "validate_pair", "LeafKind", "OpCounter", "Plan", "alpha_fft", "combine", "dft_matrix", "leaf_block_sum",
     "naive_forward", "plan", "predicted_adds", "predicted_mults", "transform_samples", "AsxCudaError",
-    "LIB_PATH",
+    "LIB_PATH", "PaddedSignal", "aliased_reconstruct", "naive_inverse", "orthogonality_kernel", "standard_fft",
+    "zero_pad",
 ]

@@ -179,6 +179,7 @@ class Plan:
         if xb.shape[-1] != self.n:
             raise ValueError(f"plan is for N={self.n}, got {tuple(x.shape)} samples")
         want = getattr(torch, np.dtype(self._in_dtype()).name)
+        xb = xb.resolve_conj().resolve_neg()  # lazy conj/neg views would hand the kernel raw memory
         if xb.dtype != want:
             xb = xb.to(want)
         if xb.stride(-1) != 1:

@@ -60,6 +60,21 @@ def kat() -> dict:
     for k, t in enumerate(p.twiddles):
         out[f"twiddle_16_4_{k}"] = np.array(t)
     out["dft_matrix_12_2_3"] = ref.dft_matrix(12, ref.DenseFactor(2, 3))
+    # inverse transform and comparators
+    for (n, p, q) in [(8, 1, 1), (8, 2, 1), (16, 4, 1), (12, 3, 2), (16, 1, 4), (12, 1, 3), (64, 1, 1)]:
+        rng = np.random.default_rng(1000 + n + 10 * p + q)
+        x = random_unit_disk(rng, n)
+        spec = ref.naive_forward(ref.Signal(x, duration=2.0), ref.DenseFactor(p, q))
+        out[f"inv_n{n}_p{p}_q{q}_X"] = spec.bins
+        out[f"inv_n{n}_p{p}_q{q}_x"] = ref.naive_inverse(spec).samples
+        if p < q:
+            out[f"alias_n{n}_p{p}_q{q}"] = ref.aliased_reconstruct(ref.Signal(x), ref.DenseFactor(p, q))
+            out[f"alias_n{n}_p{p}_q{q}_in"] = x
+    rng = np.random.default_rng(21)
+    x = random_unit_disk(rng, 32)
+    out["zeropad_x"] = x
+    out["zeropad_X"] = ref.standard_fft(ref.zero_pad(ref.Signal(x), ref.DenseFactor(4))).bins
+    out["orth_12_3_2"] = np.array([ref.orthogonality_kernel(d, 0, 12, ref.DenseFactor(3, 2)) for d in range(-11, 12)])
     return out
 
 

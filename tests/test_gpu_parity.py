@@ -337,3 +337,12 @@ def test_config2_full_size(asx):
         idx = (b * nn) % L
         want_b = np.sum(x * np.exp(-2j * np.pi * idx / L))
         assert abs(got[0, b] - want_b) <= TOL64 * np.max(np.abs(got))
+
+
+def test_lazy_conjugate_views_are_resolved(asx, torch):
+    rng = np.random.default_rng(8)
+    x = torch.from_numpy(np.stack([orc.unit_disk(rng, 64) for _ in range(3)])).cuda()
+    p = asx.plan(64, asx.DenseFactor(2), m=64)
+    got = p.execute(x.conj()).cpu().numpy()
+    want = orc.direct(np.conj(x.cpu().numpy()), 1, 2, 64)
+    assert orc.rel_err(got, want) <= TOL64
