@@ -16,6 +16,7 @@
 
 #include "../../include/asx.h"
 #include "asx_large.cuh"
+#include "asx_chirp2h.cuh"
 
 using namespace asx;
 
@@ -100,6 +101,10 @@ struct asx_plan_s {
   int64_t P1 = 0, P2 = 0;
   int lfBig = 0;
   size_t off_twP1 = 0, off_twBig = 0, off_A = 0;
+  // chirp "two halves" kernel (P = 2Q split into even/odd Q-point FFTs)
+  int half = 0;
+  int half_grid = 0;
+  size_t off_twQ = 0, off_cw = 0, off_cwc = 0, off_scratch = 0;
   LaunchEnv env;
   // execute_host resources
   std::mutex host_mtx;
@@ -213,9 +218,12 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
   const int64_t grid = std::min<int64_t>(need, int64_t(env.sms) * per_sm);
   kp.batch = batch;
   int tm_used = 0;
-  if constexpr (KIND == KIND_CHIRP && G::TPB == 1 && TmemCfg<Real, G::NT, G::R>::OK) {
-    using TMC = TmemCfg<Real, G::NT, G::R>;
-    if (env.use_tmem && per_sm * TMC::NCOLS <= 512) {
+  if constexpr (KIND == KIND_CHIRP && G::TPB == 1 &&
+                TmemCfg<Real, G::NT, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>::OK) {
+    using TMC = TmemCfg<Real, G::NT, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>;
+    using LT = PersistLayout<Real, P, G::NT, G::TPB, true>;
+    if (env.use_tmem && per_sm * TMC::NCOLS <= 512 && 2 * kp.m <= P &&
+        LT::total(row_bytes, kp.staged != 0, kp.tw_elems) <= smem) {
       auto kern_tm = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, true>;
       static thread_local int tm_attr_for = -1;
       if (tm_attr_for != dev) {
@@ -337,6 +345,51 @@ cudaError_t launch_large(int dbl, int64_t P1, int mode_cols, int mode_rows, int 
   return dbl ? launch_rows<double>(mode_rows, P1, lp, st) : launch_rows<float>(mode_rows, P1, lp, st);
 }
 
+template <typename Real, int Q, int NT>
+auto chirp2h_kernel() {
+  return k_chirp2h<Real, Q, NT>;
+}
+
+// Resident CTAs per SM of the two-halves kernel for this precision (0 if n/a).
+int chirp2h_occupancy(int dbl) {
+  int v = 0;
+  if (dbl) {
+    auto k = chirp2h_kernel<double, 4096, 512>();
+    using G = Chirp2hCfg<double, 4096, 512>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 512, G::SMEM) != cudaSuccess)
+      v = 0;
+  } else {
+    auto k = chirp2h_kernel<float, 8192, 512>();
+    using G = Chirp2hCfg<float, 8192, 512>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 512, G::SMEM) != cudaSuccess)
+      v = 0;
+  }
+  cudaGetLastError();
+  if (const char* f = std::getenv("ASX_2H_PER_SM")) v = std::atoi(f);  // tuning override
+  return v;
+}
+
+cudaError_t launch_chirp2h(int dbl, const KParams& kp, int grid, void* scratch, const void* cw, const void* cwc,
+                           cudaStream_t st) {
+  if (dbl) {
+    using G = Chirp2hCfg<double, 4096, 512>;
+    k_chirp2h<double, 4096, 512><<<grid, 512, G::SMEM, st>>>(kp, scratch, cw, cwc);
+  } else {
+    using G = Chirp2hCfg<float, 8192, 512>;
+    k_chirp2h<float, 8192, 512><<<grid, 512, G::SMEM, st>>>(kp, scratch, cw, cwc);
+  }
+  g_last_launch.grid = grid;
+  g_last_launch.block = 512;
+  g_last_launch.smem = (int)(dbl ? Chirp2hCfg<double, 4096, 512>::SMEM : Chirp2hCfg<float, 8192, 512>::SMEM);
+  g_last_launch.staged = 4;  // bit 2: two-halves kernel
+  g_last_launch.tmem = 1;
+  return cudaGetLastError();
+}
+
 int two_level_lf(int64_t L) { return (log2i(L) + 1) / 2; }
 
 // Builds [fine(F) | coarse(ceil(L/F))] for W_L at dst.
@@ -429,6 +482,12 @@ int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int6
         k_direct<double><<<grid, 256, 0, st>>>(kp);
     }
     e = cudaGetLastError();
+  } else if (p->half) {
+    char* base = static_cast<char*>(p->tables);
+    kp.twP = base + p->off_twQ;
+    const int grid = (int)std::min<int64_t>(batch, p->half_grid);
+    e = launch_chirp2h(p->dtype == ASX_C128, kp, grid, base + p->off_scratch, base + p->off_cw,
+                       base + p->off_cwc, st);
   } else if (p->large) {
     char* base = static_cast<char*>(p->tables);
     LParams lp;
@@ -638,6 +697,27 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     H_sz = p->P;
   }
   int64_t twP1_sz = 0, twBig_sz = 0, A_sz = 0;
+  int64_t twQ_sz = 0, cw_sz = 0, cwc_sz = 0, scratch_sz = 0;
+  {
+    // opt-in: measured slower than the one-CTA-per-SM kernel
+    const char* use2h = std::getenv("ASX_USE_2H");
+    const bool allow = use2h && use2h[0] == '1';
+    const int64_t Phalf_ok = (dtype == ASX_C64) ? 16384 : 8192;
+    if (allow && chosen == ASX_CHIRP && !chirp_large && chirp_P == Phalf_ok && 2 * n <= chirp_P &&
+        2 * m <= chirp_P) {
+      DeviceGuard g2(device);
+      const int occ = g2.ok ? chirp2h_occupancy(dtype == ASX_C128) : 0;
+      if (occ >= 1) {
+        p->half = 1;
+        p->half_grid = p->env.sms * occ;
+        const int64_t Q = chirp_P / 2;
+        twQ_sz = two_level_size(Q, lf_of_P((int)Q));
+        cw_sz = n;
+        cwc_sz = m;
+        scratch_sz = (int64_t)p->half_grid * Q;
+      }
+    }
+  }
   if (chosen == ASX_CHIRP && chirp_large) {
     p->large = 1;
     p->P2 = maxP;
@@ -667,6 +747,14 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   elems += align(twBig_sz);
   p->off_A = elems * es;
   elems += align(A_sz);
+  p->off_twQ = elems * es;
+  elems += align(twQ_sz);
+  p->off_cw = elems * es;
+  elems += align(cw_sz);
+  p->off_cwc = elems * es;
+  elems += align(cwc_sz);
+  p->off_scratch = elems * es;
+  elems += align(scratch_sz);
   p->table_bytes = std::max<size_t>(elems * es, 64);
 
   cudaError_t e = cudaMalloc(&p->tables, p->table_bytes);
@@ -685,6 +773,13 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   if (twP_sz) fill_two_level(base + p->off_twP, p->large ? p->P2 : p->P, lf_of_P(p->large ? (int)p->P2 : p->P), dbl, st);
   if (twP1_sz) fill_two_level(base + p->off_twP1, p->P1, lf_of_P((int)p->P1), dbl, st);
   if (twBig_sz) fill_two_level(base + p->off_twBig, chirp_P, p->lfBig, dbl, st);
+  if (twQ_sz) fill_two_level(base + p->off_twQ, chirp_P / 2, lf_of_P((int)(chirp_P / 2)), dbl, st);
+  if (p->half) {
+    const uint64_t L2 = 2ull * (uint64_t)d * (uint64_t)n;
+    const int64_t cnt = std::max(n, m);
+    k_fill_chirp_tw<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 4096), 256, 0, st>>>(
+        base + p->off_cw, base + p->off_cwc, n, m, (uint64_t)a, L2, (uint64_t)chirp_P, dbl);
+  }
   if (twA_sz) fill_two_level(base + p->off_twA, p->r * p->P, p->lfA, dbl, st);
   double2* wP_d = nullptr;
   if (chosen == ASX_CHIRP) {

@@ -13,6 +13,9 @@
 
 #include "asx_engine.cuh"
 
+#ifndef ASX_AFFT_RESEED
+#define ASX_AFFT_RESEED 4  // α-FFT pre-twiddle: exact table value every N elements, chained between
+#endif
 #ifndef ASX_ZERO_PRUNE
 #define ASX_ZERO_PRUNE 1  // chirp: compile-time zero upper half of the FFT input
 #endif
@@ -70,9 +73,9 @@ __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + 
 
 // Shared-memory layout of the persistent FFT-family kernels (host and device
 // agree on it through this helper).
-template <typename Real, int P, int NT, int TPB>
+template <typename Real, int P, int NT, int TPB, bool TS = false>
 struct PersistLayout {
-  using E = Fft<Real, P, NT>;
+  using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS>;
   using C = typename CT<Real>::T;
   static constexpr size_t FFT_BYTES = align_up(size_t(TPB) * E::SMEM_ELEMS * sizeof(C), 128);
   __host__ __device__ static size_t stage_bytes(size_t row_bytes, bool staged) {
@@ -122,10 +125,12 @@ enum { KIND_AFFT = 0, KIND_CHIRP = 1 };
 // TMEM layout of the chirp tables (TM variant, TPB == 1, NT % 128 == 0): warp
 // w owns lanes 32*(w%4).., column slot w/4 of CPT columns: H[t + NT*j] for
 // j < R, then chirp[t + NT*j] for j < R.
-template <typename Real, int NT, int R>
+template <typename Real, int NT, int R, int SEEDCOLS = 0>
 struct TmemCfg {
   static constexpr int WPC = sizeof(typename CT<Real>::T) / 4;  // 32-bit words per complex
-  static constexpr int CPT = 2 * R * WPC;                       // columns per thread
+  static constexpr int RH = R > 1 ? R / 2 : 1;                  // chirp values kept (M <= P/2)
+  static constexpr int SEED_OFF = (R + RH) * WPC;
+  static constexpr int CPT = SEED_OFF + SEEDCOLS;               // columns per thread
   static constexpr int CPC = 8 / WPC;                           // complex per 8-column access
   static constexpr int NEED = (NT / 128) * CPT;
   static constexpr int NCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
@@ -134,8 +139,9 @@ struct TmemCfg {
 
 template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
-  using E = Fft<Real, P, NT>;
-  using L = PersistLayout<Real, P, NT, TPB>;
+  constexpr bool TS = TM && KIND == KIND_CHIRP;  // last-pass twiddle seeds in TMEM too
+  using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS>;
+  using L = PersistLayout<Real, P, NT, TPB, TS>;
   using C = typename CT<Real>::T;
   constexpr int R = E::R;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
                       smraw + align_up(L::tw_off(row_bytes, staged) + p.tw_elems * sizeof(C), 16)) + team;
 
   // per-thread pass twiddles -> registers; α pre-twiddle table -> shared
-  const typename E::TwRegs tr =
+  typename E::TwRegs tr =
       E::make_tw(t, reinterpret_cast<const C*>(p.twP), reinterpret_cast<C*>(smraw + L::tab_off(row_bytes, staged)),
                  threadIdx.x, NT * TPB);
   {
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   uint32_t phase = 0;
   const C* chirp = reinterpret_cast<const C*>(p.chirp);
   const C* H = reinterpret_cast<const C*>(p.H);
-  using TMC = TmemCfg<Real, NT, R>;
+  using TMC = TmemCfg<Real, NT, R, E::TSEED_COLS>;
   uint32_t tbase = 0;
   uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar - team + TPB + 1);  // after the mbarriers
   if constexpr (TM) {
@@ -195,11 +201,14 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
       for (int k = 0; k < TMC::CPC; ++k) {
         const int idx = t + NT * (j0 + k);
         c_to_words(__ldg(H + idx), &wh[k * TMC::WPC]);
-        c_to_words(idx < p.chirp_len ? __ldg(chirp + idx) : mk(Real(0), Real(0)), &wc[k * TMC::WPC]);
+        c_to_words((j0 + k < TMC::RH && idx < p.chirp_len) ? __ldg(chirp + idx) : mk(Real(0), Real(0)),
+                   &wc[k * TMC::WPC]);
       }
       tmem_st8(tbase + j0 * TMC::WPC, wh);
-      tmem_st8(tbase + (R + j0) * TMC::WPC, wc);
+      if (j0 < TMC::RH) tmem_st8(tbase + (R + j0) * TMC::WPC, wc);
     }
+    E::store_tmem_seeds(t, tbase + TMC::SEED_OFF);
+    tr.tseed = tbase + TMC::SEED_OFF;
     tmem_wait_st();
   }
   // chirp / kernel-spectrum value j of this thread (TMEM or L2)
@@ -271,12 +280,13 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
       }
       if (live) {
         C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+        constexpr int ROUT = TM ? TMC::RH : R;  // TM launches need M <= P/2
 #pragma unroll
-        for (int j0 = 0; j0 < R; j0 += TMC::CPC) {
+        for (int j0 = 0; j0 < ROUT; j0 += (TMC::CPC < ROUT ? TMC::CPC : ROUT)) {
           C cw[TMC::CPC];
           tab_chunk(1, j0, cw);
 #pragma unroll
-          for (int k = 0; k < TMC::CPC && j0 + k < R; ++k) {
+          for (int k = 0; k < TMC::CPC && j0 + k < ROUT; ++k) {
             const int mm = t + NT * (j0 + k);
             if (mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
           }
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
               val = cadd(val, load_row<C>(stage, p.x, row_off, nn + int64_t(s) * P, p.real_in, staged));
           }
           if (c != 0) {
-            if (i > 0) wc = ((i & 3) == 0) ? tw_lookup_rt(twa, c * nn, p.lfA) : cmul(wc, wst);
+            if (i > 0) wc = ((i % ASX_AFFT_RESEED) == 0) ? tw_lookup_rt(twa, c * nn, p.lfA) : cmul(wc, wst);
             val = cmul(val, wc);
           }
           v[i] = val;
