@@ -43,6 +43,7 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the non-production methods")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work for the baseline sample")
     return ap.parse_args()
 
@@ -236,6 +237,32 @@ def run_gpu(args):
     achieved = bytes_step / avg_launch_s / 1e9
     flops = w.flops_alg(nloc)
 
+    # the other method(s) on the same shard, for reference (the α-FFT recursion
+    # is the paper's algorithm; `auto` picks the cheapest for the config)
+    alt = {}
+    if not args.no_alt:
+        for meth in ("fft", "chirp", "direct"):
+            if meth == plan.method:
+                continue
+            try:
+                q = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, method=meth, real_input=w.real, device=local)
+            except Exception:
+                continue
+            if meth == "direct" and w.n * w.m * nloc > 2e12:
+                continue
+            q.execute(x, out=out)
+            torch.cuda.synchronize()
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, min(args.steps, 10))
+            s_.record(stream)
+            for _ in range(reps):
+                q.execute(x, out=out)
+            e_.record(stream)
+            torch.cuda.synchronize()
+            alt[meth] = {"ms_per_step": s_.elapsed_time(e_) / reps, "fft_size": q.fft_size}
+        plan.execute(x, out=out)  # leave the production result in `out`
+        torch.cuda.synchronize()
+
     # e2e through the C ABI with host buffers (H2D + transform + D2H inside)
     e2e = None
     if not args.no_e2e:
@@ -297,6 +324,7 @@ def run_gpu(args):
                 "flops_alg_per_launch": flops, "achieved_alg_tflops": flops / avg_launch_s / 1e12,
                 "kernel": {"fft": "k_afft", "chirp": "k_chirp", "direct": "k_direct"}[plan.method],
             },
+            "other_methods": alt,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * int(plan.info.kernels_per_execute),
