@@ -1,0 +1,169 @@
+"""Command line, GPU-backed: ``python -m paper_2403_16665_b200``.
+
+Mirrors the reference's ``alpha-spectra`` front end (ref/cli.py:1-13) for the
+transform path: ``compute`` (file -> spectrum file), ``verify`` (the
+cross-checking suites), ``bench`` (device-time grid over N x alpha x method).
+Exit codes are the reference's: 0 ok, 1 verification failure, 2 parse error,
+3 alpha incompatible with N, 4 size unsupported by the method, 5 claim failure.
+``--method auto`` never falls back to a CPU path: it picks among the GPU
+methods (α-FFT, chirp-z, direct).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+
+from . import fileio, verify
+from .core import DenseFactor, IncompatibleAlphaError, Signal, Spectrum, UnsupportedSizeError
+
+EXIT_OK, EXIT_VERIFY_FAILED, EXIT_PARSE_ERROR, EXIT_BAD_ALPHA, EXIT_BAD_SIZE, EXIT_CLAIM_FAILED = 0, 1, 2, 3, 4, 5
+
+
+def _alpha(text):
+    try:
+        return DenseFactor.from_string(text)
+    except ValueError as exc:
+        raise argparse.ArgumentTypeError(str(exc)) from None
+
+
+def _ints(text):
+    try:
+        vals = [int(v) for v in text.split(",") if v.strip()]
+    except ValueError:
+        raise argparse.ArgumentTypeError(f"expected comma-separated integers, got {text!r}") from None
+    if not vals:
+        raise argparse.ArgumentTypeError("list must not be empty")
+    return vals
+
+
+def _alphas(text):
+    try:
+        return [DenseFactor.from_string(v) for v in text.split(",") if v.strip()]
+    except ValueError as exc:
+        raise argparse.ArgumentTypeError(str(exc)) from None
+
+
+def build_parser() -> argparse.ArgumentParser:
+    ap = argparse.ArgumentParser(prog="paper_2403_16665_b200",
+                                 description="GPU α-DFT / α-FFT: spectra with bin density alpha = p/q.")
+    sub = ap.add_subparsers(dest="command", required=True)
+    c = sub.add_parser("compute", help="transform a signal file into a spectrum file")
+    c.add_argument("--input", required=True)
+    c.add_argument("--output", required=True)
+    c.add_argument("--alpha", type=_alpha, default=DenseFactor(1), help="density p/q (default 1/1)")
+    c.add_argument("--method", choices=("auto", "fft", "naive", "zeropad", "chirp"), default="auto")
+    c.add_argument("--bins", type=int, default=None, help="explicit bin count M (default alpha*N)")
+    c.add_argument("--duration", type=float, default=None)
+    v = sub.add_parser("verify", help="run the numerical cross-checking suites on the GPU")
+    v.add_argument("--seed", type=int, default=0)
+    v.add_argument("--sizes", type=_ints, default=list(verify.DEFAULT_SIZES))
+    v.add_argument("--inject-fault", action="store_true", help=argparse.SUPPRESS)
+    b = sub.add_parser("bench", help="device-time grid over N x alpha x method")
+    b.add_argument("--grid-n", type=_ints, default=[256, 1024, 4096])
+    b.add_argument("--grid-alpha", type=_alphas, default=[DenseFactor(1), DenseFactor(2), DenseFactor(8)])
+    b.add_argument("--methods", default="fft,chirp,direct")
+    b.add_argument("--batch", type=int, default=256)
+    b.add_argument("--reps", type=int, default=10)
+    b.add_argument("--output", default=None, help="JSON report path")
+    return ap
+
+
+def cmd_compute(args) -> int:
+    from . import comparators, transforms
+
+    try:
+        signal = fileio.read_signal(args.input)
+    except FileNotFoundError:
+        print(f"error: no such file: {args.input}", file=sys.stderr)
+        return EXIT_PARSE_ERROR
+    except fileio.SignalParseError as exc:
+        print(f"error: {args.input}: {exc}", file=sys.stderr)
+        return EXIT_PARSE_ERROR
+    if args.duration is not None:
+        signal = Signal(signal.samples, args.duration)
+    alpha, n = args.alpha, len(signal)
+    try:
+        if args.method == "naive":
+            spec, used = transforms.naive_forward(signal, alpha, m=args.bins), "naive"
+        elif args.method == "zeropad":
+            if alpha.p < alpha.q:
+                print(f"error: zero-padding needs alpha >= 1, got {alpha}", file=sys.stderr)
+                return EXIT_BAD_ALPHA
+            padded = comparators.standard_fft(comparators.zero_pad(signal, alpha))
+            spec, used = Spectrum(padded.bins, n, alpha, signal.duration), "zeropad"
+        else:
+            p = transforms.plan(n, alpha, m=args.bins, method=args.method)
+            spec, used = transforms.alpha_fft(signal, p), p.method
+    except IncompatibleAlphaError as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return EXIT_BAD_ALPHA
+    except UnsupportedSizeError as exc:
+        print(f"error: {exc} (try --method auto)", file=sys.stderr)
+        return EXIT_BAD_SIZE
+    fileio.write_spectrum(spec, args.output, used)
+    print(f"wrote {spec.m} bins (N={n}, alpha={alpha}, method={used}) to {args.output}")
+    return EXIT_OK
+
+
+def cmd_verify(args) -> int:
+    results = verify.run_all(seed=args.seed, sizes=args.sizes, inject_fault=args.inject_fault)
+    failed = [r for r in results if not r.passed]
+    for r in results:
+        print(f"{r.name}: max error {r.max_error:.3e} (tolerance {r.tolerance:.0e}, {r.cases} cases) "
+              f"{'PASS' if r.passed else 'FAIL'}")
+    for r in failed:
+        print(f"  worst case for {r.name}: {r.worst}", file=sys.stderr)
+    return EXIT_OK if not failed else EXIT_VERIFY_FAILED
+
+
+def cmd_bench(args) -> int:
+    import torch
+
+    from . import transforms
+
+    records = []
+    for n in args.grid_n:
+        for alpha in args.grid_alpha:
+            if (n * alpha.p) % alpha.q:
+                continue
+            m = n * alpha.p // alpha.q
+            x = torch.randn((args.batch, n), dtype=torch.complex128, device="cuda")
+            for method in [s.strip() for s in args.methods.split(",") if s.strip()]:
+                try:
+                    p = transforms.plan(n, alpha, method=method)
+                except (UnsupportedSizeError, ValueError) as exc:
+                    records.append({"N": n, "alpha": str(alpha), "method": method, "skipped": str(exc)[:80]})
+                    continue
+                out = torch.empty((args.batch, m), dtype=torch.complex128, device="cuda")
+                for _ in range(3):
+                    p.execute(x, out=out)
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                for _ in range(args.reps):
+                    p.execute(x, out=out)
+                e.record()
+                torch.cuda.synchronize()
+                ms = s.elapsed_time(e) / args.reps
+                records.append({"N": n, "alpha": str(alpha), "method": method, "batch": args.batch,
+                                "ms": ms, "points_per_s": args.batch * m / (ms / 1e3),
+                                "mults": p.predicted_mults, "adds": p.predicted_adds})
+                print(json.dumps(records[-1]))
+    if not any("ms" in r for r in records):
+        print("error: no runnable grid cells", file=sys.stderr)
+        return EXIT_PARSE_ERROR
+    if args.output:
+        with open(args.output, "w") as fh:
+            json.dump({"records": records}, fh, indent=1)
+    return EXIT_OK
+
+
+def main(argv=None) -> int:
+    args = build_parser().parse_args(argv)
+    return {"compute": cmd_compute, "verify": cmd_verify, "bench": cmd_bench}[args.command](args)
+
+
+def entry() -> None:
+    sys.exit(main())

@@ -116,7 +116,7 @@ def aliased_reconstruct(signal: Signal, alpha: DenseFactor) -> np.ndarray:
     dev = _default_device()
     k = -(-n // m)
     x = torch.zeros(k * m, dtype=torch.complex128, device=f"cuda:{dev}")
-    x[:n] = torch.from_numpy(signal.samples).to(x.device)
+    x[:n] = torch.from_numpy(np.array(signal.samples)).to(x.device)
     cols = x.view(k, m).t().contiguous()  # row r = the samples with residue r
     folded = torch.empty(m, dtype=torch.complex128, device=x.device)
     st = torch.cuda.current_stream(dev).cuda_stream

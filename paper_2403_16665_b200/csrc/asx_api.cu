@@ -137,6 +137,12 @@ size_t in_elem(const asx_plan_s* p) {
 #ifndef ASX_R_4K_C128
 #define ASX_R_4K_C128 8  // values per thread for c128 P == 4096
 #endif
+#ifndef ASX_KR_C128_4K
+#define ASX_KR_C128_4K 1
+#endif
+#ifndef ASX_KR_C64_8K
+#define ASX_KR_C64_8K 1
+#endif
 #ifndef ASX_MT_C64
 #define ASX_MT_C64 1024  // threads per SM the register budget targets (c64)
 #endif
@@ -153,6 +159,8 @@ template <int P, typename Real> struct Cfg {
   static constexpr int TPB = (NT == 1) ? 64 : (NT >= 256 ? 1 : 256 / NT);
   static constexpr int MT = DBL ? ASX_MT_C128 : ASX_MT_C64;
   static constexpr int MINB = (MT / (NT * TPB)) > 1 ? (MT / (NT * TPB)) : 1;
+  // α-FFT residues transformed together per thread (ILP for the latency-bound FP64 case)
+  static constexpr int KR = (DBL && P == 4096) ? ASX_KR_C128_4K : ((!DBL && P == 8192) ? ASX_KR_C64_8K : 1);
 };
 
 template <typename KernelT>
@@ -164,10 +172,11 @@ cudaError_t prep_smem(KernelT kern, size_t smem) {
 template <typename Real, int P, int KIND>
 cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const LaunchEnv& env) {
   using G = Cfg<P, Real>;
-  using L = PersistLayout<Real, P, G::NT, G::TPB>;
+  constexpr int KR = KIND == KIND_AFFT ? G::KR : 1;
+  using L = PersistLayout<Real, P, G::NT, G::TPB, false, KR>;
   if (batch == 0) return cudaSuccess;
   const size_t row_bytes = size_t(kp.n) * (kp.real_in ? sizeof(Real) : 2 * sizeof(Real));
-  auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB>;
+  auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR>;
   // one-time opt-in to the full shared-memory carve-out for this kernel
   static thread_local int attr_set_for = -1;
   int dev = 0;

@@ -73,11 +73,11 @@ __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + 
 
 // Shared-memory layout of the persistent FFT-family kernels (host and device
 // agree on it through this helper).
-template <typename Real, int P, int NT, int TPB, bool TS = false>
+template <typename Real, int P, int NT, int TPB, bool TS = false, int KR = 1>
 struct PersistLayout {
   using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS>;
   using C = typename CT<Real>::T;
-  static constexpr size_t FFT_BYTES = align_up(size_t(TPB) * E::SMEM_ELEMS * sizeof(C), 128);
+  static constexpr size_t FFT_BYTES = align_up(size_t(TPB) * KR * E::SMEM_ELEMS * sizeof(C), 128);
   __host__ __device__ static size_t stage_bytes(size_t row_bytes, bool staged) {
     return staged ? align_up(row_bytes, 128) : 0;
   }
@@ -137,18 +137,18 @@ struct TmemCfg {
   static constexpr bool OK = (NT % 128 == 0) && NEED <= 512;
 };
 
-template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false>
+template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   constexpr bool TS = TM && KIND == KIND_CHIRP;  // last-pass twiddle seeds in TMEM too
   using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS>;
-  using L = PersistLayout<Real, P, NT, TPB, TS>;
+  using L = PersistLayout<Real, P, NT, TPB, TS, KR>;
   using C = typename CT<Real>::T;
   constexpr int R = E::R;
   extern __shared__ __align__(128) unsigned char smraw[];
   const int team = threadIdx.x / NT, t = threadIdx.x % NT;
   const bool staged = p.staged != 0;
   const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(Real) : sizeof(C));
-  C* fbuf = reinterpret_cast<C*>(smraw) + team * E::SMEM_ELEMS;
+  C* fbuf = reinterpret_cast<C*>(smraw) + team * KR * E::SMEM_ELEMS;
   unsigned char* stage = smraw + L::FFT_BYTES + team * L::stage_bytes(row_bytes, staged);
   C* twa = reinterpret_cast<C*>(smraw + L::tw_off(row_bytes, staged));  // α pre-twiddle W_{rN} (afft, r > 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(
@@ -297,31 +297,37 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         mbar_wait(bar, phase);
         phase ^= 1;
       }
-      for (int c = 0; c < p.r; ++c) {
-        C v[R];
-        // W_{rN}^{c n}, n = t + NT*i: base W^{c t} times step W^{c NT} chained
-        // over i, re-seeded from the shared table every 4 steps.
-        C wst = mk(Real(1), Real(0)), wc = wst;
-        if (c != 0) {
-          wst = tw_lookup_rt(twa, c * NT, p.lfA);
-          wc = tw_lookup_rt(twa, c * t, p.lfA);
-        }
+      // KR output residues at a time: their transforms share twiddles and
+      // barriers and interleave in the pipeline (ILP)
+      for (int c0 = 0; c0 < p.r; c0 += KR) {
+        C v[KR][R];
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const int nn = t + NT * i;
-          C val = mk(Real(0), Real(0));
-          if (live) {
-            val = load_row<C>(stage, p.x, row_off, nn, p.real_in, staged);
-            for (int s = 1; s < p.fold; ++s)
-              val = cadd(val, load_row<C>(stage, p.x, row_off, nn + int64_t(s) * P, p.real_in, staged));
+        for (int k = 0; k < KR; ++k) {
+          const int c = c0 + k;
+          // W_{rN}^{c n}, n = t + NT*i: base W^{c t} times step W^{c NT} chained
+          // over i, re-seeded from the shared table every ASX_AFFT_RESEED steps.
+          C wst = mk(Real(1), Real(0)), wc = wst;
+          if (c != 0 && c < p.r) {
+            wst = tw_lookup_rt(twa, c * NT, p.lfA);
+            wc = tw_lookup_rt(twa, c * t, p.lfA);
           }
-          if (c != 0) {
-            if (i > 0) wc = ((i % ASX_AFFT_RESEED) == 0) ? tw_lookup_rt(twa, c * nn, p.lfA) : cmul(wc, wst);
-            val = cmul(val, wc);
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            const int nn = t + NT * i;
+            C val = mk(Real(0), Real(0));
+            if (live && c < p.r) {
+              val = load_row<C>(stage, p.x, row_off, nn, p.real_in, staged);
+              for (int s = 1; s < p.fold; ++s)
+                val = cadd(val, load_row<C>(stage, p.x, row_off, nn + int64_t(s) * P, p.real_in, staged));
+            }
+            if (c != 0) {
+              if (i > 0) wc = ((i % ASX_AFFT_RESEED) == 0) ? tw_lookup_rt(twa, c * nn, p.lfA) : cmul(wc, wst);
+              val = cmul(val, wc);
+            }
+            v[k][i] = val;
           }
-          v[i] = val;
         }
-        if (staged && c == p.r - 1) {
+        if (staged && c0 + KR >= p.r) {
           __syncthreads();
           if (t == 0 && u + stride < batch) {
             fence_proxy_async();
@@ -331,14 +337,19 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
                         (uint32_t)row_bytes, bar);
           }
         }
-        E::run(v, fbuf, t, tr, xs);
+        E::template run<KR>(v, fbuf, t, tr, xs);
         if (live) {
           C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
           const int64_t period = p.r * P;
 #pragma unroll
-          for (int i = 0; i < R; ++i) {
-            const int d = t + NT * i;
-            for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = v[i];
+          for (int k = 0; k < KR; ++k) {
+            const int c = c0 + k;
+            if (c >= p.r) continue;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              const int d = t + NT * i;
+              for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = v[k][i];
+            }
           }
         }
       }

@@ -94,3 +94,35 @@ def test_standard_fft_is_numpy_fft(asx):
     assert np.max(np.abs(asx.standard_fft(x).bins - np.fft.fft(x))) < 1e-11
     x = orc.unit_disk(rng, 100)  # non-power-of-two: chirp path
     assert np.max(np.abs(asx.standard_fft(x).bins - np.fft.fft(x))) < 1e-11
+
+
+def test_cli_compute_and_verify(asx, tmp_path, golden_configs):
+    from paper_2403_16665_b200 import cli, fileio
+
+    sig = asx.Signal(golden_configs["c0_x"])
+    src = tmp_path / "sig.csv"
+    fileio.write_signal_csv(sig, src)
+    for method in ("auto", "fft", "naive", "zeropad", "chirp"):
+        out = tmp_path / f"spec_{method}.csv"
+        assert cli.main(["compute", "--input", str(src), "--output", str(out), "--alpha", "4",
+                         "--method", method]) == 0
+        spec, used = fileio.read_spectrum(out)
+        assert spec.m == 4096
+        assert np.max(np.abs(spec.bins[:1024] - golden_configs["c0_naive"])) / np.max(
+            np.abs(golden_configs["c0_naive"])) < 1e-10
+    # explicit bin count (BASELINE's M = N) and an alpha the reference rejects
+    out = tmp_path / "m.csv"
+    assert cli.main(["compute", "--input", str(src), "--output", str(out), "--alpha", "100/37",
+                     "--bins", "1024"]) == 0
+    assert cli.main(["compute", "--input", str(src), "--output", str(out), "--alpha", "100/37"]) == 3
+    assert cli.main(["compute", "--input", str(src), "--output", str(out), "--alpha", "3/2",
+                     "--method", "fft"]) == 4
+    assert cli.main(["verify", "--sizes", "2,4,8,16"]) == 0
+    assert cli.main(["verify", "--sizes", "4", "--inject-fault"]) == 1
+
+
+def test_gpu_verify_suites(asx):
+    from paper_2403_16665_b200 import verify
+
+    for r in verify.run_all(seed=0):
+        assert r.passed, (r.name, r.max_error, r.worst)
