@@ -227,9 +227,9 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
   const int64_t grid = std::min<int64_t>(need, int64_t(env.sms) * per_sm);
   kp.batch = batch;
   int tm_used = 0;
-  if constexpr (KIND == KIND_CHIRP && G::TPB == 1 &&
-                TmemCfg<Real, G::NT, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>::OK) {
-    using TMC = TmemCfg<Real, G::NT, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>;
+  if constexpr (KIND == KIND_CHIRP && G::NT > 1 &&
+                TmemCfg<Real, G::NT * G::TPB, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>::OK) {
+    using TMC = TmemCfg<Real, G::NT * G::TPB, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>;
     using LT = PersistLayout<Real, P, G::NT, G::TPB, true>;
     if (env.use_tmem && per_sm * TMC::NCOLS <= 512 && 2 * kp.m <= P &&
         LT::total(row_bytes, kp.staged != 0, kp.tw_elems) <= smem) {

@@ -122,19 +122,19 @@ struct PersistLayout {
 // ---------------------------------------------------------------------------
 enum { KIND_AFFT = 0, KIND_CHIRP = 1 };
 
-// TMEM layout of the chirp tables (TM variant, TPB == 1, NT % 128 == 0): warp
+// TMEM layout of the chirp tables (TM variant; CTA size NTH % 128 == 0): warp
 // w owns lanes 32*(w%4).., column slot w/4 of CPT columns: H[t + NT*j] for
 // j < R, then chirp[t + NT*j] for j < R.
-template <typename Real, int NT, int R, int SEEDCOLS = 0>
+template <typename Real, int NTH, int R, int SEEDCOLS = 0>
 struct TmemCfg {
   static constexpr int WPC = sizeof(typename CT<Real>::T) / 4;  // 32-bit words per complex
   static constexpr int RH = R > 1 ? R / 2 : 1;                  // chirp values kept (M <= P/2)
   static constexpr int SEED_OFF = (R + RH) * WPC;
   static constexpr int CPT = SEED_OFF + SEEDCOLS;               // columns per thread
   static constexpr int CPC = 8 / WPC;                           // complex per 8-column access
-  static constexpr int NEED = (NT / 128) * CPT;
+  static constexpr int NEED = (NTH / 128) * CPT;
   static constexpr int NCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr bool OK = (NT % 128 == 0) && NEED <= 512;
+  static constexpr bool OK = (NTH % 128 == 0) && NEED <= 512;
 };
 
 template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1>
@@ -183,11 +183,11 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   uint32_t phase = 0;
   const C* chirp = reinterpret_cast<const C*>(p.chirp);
   const C* H = reinterpret_cast<const C*>(p.H);
-  using TMC = TmemCfg<Real, NT, R, E::TSEED_COLS>;
+  using TMC = TmemCfg<Real, NT * TPB, R, E::TSEED_COLS>;
   uint32_t tbase = 0;
   uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar - team + TPB + 1);  // after the mbarriers
   if constexpr (TM) {
-    static_assert(TPB == 1 && TMC::OK, "TMEM tables need one team per CTA");
+    static_assert(TMC::OK, "TMEM tables need a CTA of 128k threads within 512 columns");
     const int warp = threadIdx.x >> 5;
     if (warp == 0) tmem_alloc(&tmem_slot, TMC::NCOLS);
     tmem_fence_before();
@@ -278,7 +278,9 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
           }
         }
       }
-      if (live) {
+      {
+        // table loads stay outside `live`: tcgen05.ld is warp-collective and a
+        // warp may span several teams when NT < 32
         C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
         constexpr int ROUT = TM ? TMC::RH : R;  // TM launches need M <= P/2
 #pragma unroll
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
 #pragma unroll
           for (int k = 0; k < TMC::CPC && j0 + k < ROUT; ++k) {
             const int mm = t + NT * (j0 + k);
-            if (mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+            if (live && mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
           }
         }
       }
