@@ -173,7 +173,8 @@ template <typename Real, int P, int KIND>
 cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const LaunchEnv& env) {
   using G = Cfg<P, Real>;
   constexpr int KR = KIND == KIND_AFFT ? G::KR : 1;
-  using L = PersistLayout<Real, P, G::NT, G::TPB, false, KR>;
+  constexpr bool DBUF = persist_dbuf<Real, P, G::NT, KIND>();
+  using L = PersistLayout<Real, P, G::NT, G::TPB, false, KR, DBUF>;
   if (batch == 0) return cudaSuccess;
   const size_t row_bytes = size_t(kp.n) * (kp.real_in ? sizeof(Real) : 2 * sizeof(Real));
   auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR>;
@@ -230,7 +231,7 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
   if constexpr (KIND == KIND_CHIRP && G::NT > 1 &&
                 TmemCfg<Real, G::NT * G::TPB, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>::OK) {
     using TMC = TmemCfg<Real, G::NT * G::TPB, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>;
-    using LT = PersistLayout<Real, P, G::NT, G::TPB, true>;
+    using LT = PersistLayout<Real, P, G::NT, G::TPB, true, 1, DBUF>;
     if (env.use_tmem && per_sm * TMC::NCOLS <= 512 && 2 * kp.m <= P &&
         LT::total(row_bytes, kp.staged != 0, kp.tw_elems) <= smem) {
       auto kern_tm = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, true>;

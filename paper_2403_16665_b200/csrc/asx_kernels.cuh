@@ -73,9 +73,14 @@ __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + 
 
 // Shared-memory layout of the persistent FFT-family kernels (host and device
 // agree on it through this helper).
-template <typename Real, int P, int NT, int TPB, bool TS = false, int KR = 1>
+template <typename Real, int P, int NT, int KIND>
+constexpr bool persist_dbuf() {
+  return KIND == 1 && size_t(P) * sizeof(typename CT<Real>::T) <= ASX_DBUF_MAX_BYTES;
+}
+
+template <typename Real, int P, int NT, int TPB, bool TS = false, int KR = 1, bool DBUF = false>
 struct PersistLayout {
-  using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS>;
+  using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS, DBUF>;
   using C = typename CT<Real>::T;
   static constexpr size_t FFT_BYTES = align_up(size_t(TPB) * KR * E::SMEM_ELEMS * sizeof(C), 128);
   __host__ __device__ static size_t stage_bytes(size_t row_bytes, bool staged) {
@@ -140,8 +145,9 @@ struct TmemCfg {
 template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   constexpr bool TS = TM && KIND == KIND_CHIRP;  // last-pass twiddle seeds in TMEM too
-  using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS>;
-  using L = PersistLayout<Real, P, NT, TPB, TS, KR>;
+  constexpr bool DBUF = persist_dbuf<Real, P, NT, KIND>();
+  using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS, DBUF>;
+  using L = PersistLayout<Real, P, NT, TPB, TS, KR, DBUF>;
   using C = typename CT<Real>::T;
   constexpr int R = E::R;
   extern __shared__ __align__(128) unsigned char smraw[];

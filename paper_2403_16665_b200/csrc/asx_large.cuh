@@ -55,8 +55,8 @@ struct ColCfg {
   static constexpr int R = P1 < 8 ? P1 : 8;
   static constexpr int NT = P1 / R;
   using E = Fft<Real, P1, NT>;
-  static constexpr size_t SMEM =
-      (size_t(kColTile) * (P1 + (P1 >> E::LPAD)) + E::TAB_ELEMS + 2) * sizeof(typename CT<Real>::T) + 16;
+  static constexpr int CS = E::SMEM_ELEMS > P1 + (P1 >> E::LPAD) ? E::SMEM_ELEMS : P1 + (P1 >> E::LPAD);
+  static constexpr size_t SMEM = (size_t(kColTile) * CS + E::TAB_ELEMS + 2) * sizeof(typename CT<Real>::T) + 16;
 };
 
 // 8 teams of NT threads, one column each; the tile passes through the teams'
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
   constexpr int THREADS = NT * kColTile;
   const int64_t P2 = p.P2;
   const uint64_t Pmask = uint64_t(p.P - 1);
-  constexpr int CS = P1 + (P1 >> E::LPAD);  // per-column tile stride (>= SMEM_ELEMS)
+  constexpr int CS = E::SMEM_ELEMS > P1 + (P1 >> E::LPAD) ? E::SMEM_ELEMS : P1 + (P1 >> E::LPAD);  // per-column stride
   extern __shared__ __align__(128) unsigned char smraw[];
   C* smbase = reinterpret_cast<C*>(smraw);
   const int team = threadIdx.x / NT, t = threadIdx.x % NT;
