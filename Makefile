@@ -1,25 +1,33 @@
 # Builds the in-tree CUDA library for sm_100a (B200).  Used by __graft_entry__.build().
+# The kernels are instantiated in separate translation units so `make -j`
+# compiles them in parallel.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr -cudart static
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $(VFLAGS)
 PKG := paper_2403_16665_b200
-SRC := $(PKG)/csrc/asx_api.cu
-HDR := $(PKG)/csrc/asx_engine.cuh $(PKG)/csrc/asx_kernels.cuh include/asx.h
+CSRC := $(PKG)/csrc
+UNITS := asx_api asx_launch_f32 asx_launch_f64 asx_launch_misc
+HDR := $(wildcard $(CSRC)/*.cuh) include/asx.h
+VNAME ?=
+BDIR := build/obj$(VNAME)
+OBJS := $(addprefix $(BDIR)/,$(addsuffix .o,$(UNITS)))
+LIB := $(PKG)/libasx$(if $(VNAME),_$(VNAME),).so
 
-all: $(PKG)/libasx.so
+all: $(LIB)
 
-$(PKG)/libasx.so: $(SRC) $(HDR)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build/ptxas.log || (cat build/ptxas.log; exit 1)
+$(BDIR)/%.o: $(CSRC)/%.cu $(HDR)
+	@mkdir -p $(BDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
 
-$(PKG)/libasx.so: | build
-build:
-	mkdir -p build
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+	@cat $(BDIR)/*.ptxas.log > build/ptxas$(if $(VNAME),_$(VNAME),).log
 
-# performance variants for tuning sweeps (scripts/sweep.py with ASX_LIB_PATH)
-variant: | build
-	$(NVCC) $(NVFLAGS) $(VFLAGS) -shared -o $(PKG)/libasx_$(VNAME).so $(SRC) 2> build/ptxas_$(VNAME).log
+# performance variants for tuning sweeps: make variant VNAME=x VFLAGS="-D..." (scripts/sweep.py with ASX_LIB_PATH)
+variant:
+	$(MAKE) VNAME=$(VNAME) VFLAGS="$(VFLAGS)" all
 
 clean:
-	rm -f $(PKG)/libasx.so
+	rm -rf build/obj* $(PKG)/libasx*.so
 
-.PHONY: all clean
+.PHONY: all clean variant

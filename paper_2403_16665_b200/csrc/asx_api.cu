@@ -15,10 +15,10 @@
 #include <string>
 
 #include "../../include/asx.h"
-#include "asx_large.cuh"
-#include "asx_chirp2h.cuh"
+#include "asx_dispatch.cuh"
 
 using namespace asx;
+using namespace asx_host;
 
 namespace {
 
@@ -67,18 +67,6 @@ int bit_length(int64_t v) {
 constexpr int kMaxP_c64 = 16384;
 constexpr int kMaxP_c128 = 8192;
 
-struct LaunchEnv {
-  int sms = 148;
-  size_t smem_optin = 227 * 1024;
-  int use_tmem = 1;  // chirp tables in tensor memory (env ASX_NO_TMEM=1 disables, for A/B runs)
-};
-
-// Shape of the most recent launch on this thread (asx_last_launch, for
-// benchmarks / tests that report occupancy decisions).
-struct LastLaunch {
-  int grid = 0, block = 0, smem = 0, staged = 0, tmem = 0;
-};
-thread_local LastLaunch g_last_launch;
 
 }  // namespace
 
@@ -137,269 +125,6 @@ size_t in_elem(const asx_plan_s* p) {
 #ifndef ASX_R_4K_C128
 #define ASX_R_4K_C128 8  // values per thread for c128 P == 4096
 #endif
-#ifndef ASX_KR_C128_4K
-#define ASX_KR_C128_4K 1
-#endif
-#ifndef ASX_KR_C64_8K
-#define ASX_KR_C64_8K 1
-#endif
-#ifndef ASX_MT_C64
-#define ASX_MT_C64 1024  // threads per SM the register budget targets (c64)
-#endif
-#ifndef ASX_MT_C128
-#define ASX_MT_C128 512  // threads per SM the register budget targets (c128)
-#endif
-template <int P, typename Real> struct Cfg {
-  static constexpr bool DBL = sizeof(Real) == 8;
-  static constexpr int R = (P <= 32)     ? P
-                           : (P <= 2048) ? 8
-                           : DBL         ? (P == 4096 ? ASX_R_4K_C128 : 16)
-                                         : (P == 16384 ? ASX_R_16K_C64 : ASX_R_BIG_C64);
-  static constexpr int NT = P / R;
-  static constexpr int TPB = (NT == 1) ? 64 : (NT >= 256 ? 1 : 256 / NT);
-  static constexpr int MT = DBL ? ASX_MT_C128 : ASX_MT_C64;
-  static constexpr int MINB = (MT / (NT * TPB)) > 1 ? (MT / (NT * TPB)) : 1;
-  // α-FFT residues transformed together per thread (ILP for the latency-bound FP64 case)
-  static constexpr int KR = (DBL && P == 4096) ? ASX_KR_C128_4K : ((!DBL && P == 8192) ? ASX_KR_C64_8K : 1);
-};
-
-template <typename KernelT>
-cudaError_t prep_smem(KernelT kern, size_t smem) {
-  if (smem > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return cudaSuccess;
-}
-
-template <typename Real, int P, int KIND>
-cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const LaunchEnv& env) {
-  using G = Cfg<P, Real>;
-  constexpr int KR = KIND == KIND_AFFT ? G::KR : 1;
-  constexpr bool DBUF = persist_dbuf<Real, P, G::NT, KIND>();
-  using L = PersistLayout<Real, P, G::NT, G::TPB, false, KR, DBUF>;
-  if (batch == 0) return cudaSuccess;
-  const size_t row_bytes = size_t(kp.n) * (kp.real_in ? sizeof(Real) : 2 * sizeof(Real));
-  auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR>;
-  // one-time opt-in to the full shared-memory carve-out for this kernel
-  static thread_local int attr_set_for = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_set_for != dev) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
-    if (e != cudaSuccess) return e;
-    attr_set_for = dev;
-  }
-  // occupancy with / without the TMA staging buffer (cached per smem size);
-  // staging is used only when it does not cost resident CTAs.
-  struct Occ {
-    size_t smem = 0;
-    int per_sm = 0;
-  };
-  static thread_local Occ cache[2];
-  auto occ = [&](int stg, size_t sm) -> int {
-    if (sm > env.smem_optin) return 0;
-    Occ& c = cache[stg];
-    if (c.smem != sm) {
-      int v = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, G::NT * G::TPB, sm) != cudaSuccess) {
-        cudaGetLastError();
-        v = 0;
-      }
-      c.smem = sm;
-      c.per_sm = v;
-    }
-    return c.per_sm;
-  };
-  if (G::NT == 1) kp.staged = 0;
-  const size_t smem_u = L::total(row_bytes, false, kp.tw_elems);
-  const int occ_u = occ(0, smem_u);
-  size_t smem = smem_u;
-  int per_sm = occ_u;
-  if (kp.staged) {
-    const size_t smem_s = L::total(row_bytes, true, kp.tw_elems);
-    const int occ_s = occ(1, smem_s);
-    if (occ_s >= occ_u && occ_s > 0) {
-      smem = smem_s;
-      per_sm = occ_s;
-    } else {
-      kp.staged = 0;
-    }
-  }
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const int64_t need = (batch + G::TPB - 1) / G::TPB;
-  const int64_t grid = std::min<int64_t>(need, int64_t(env.sms) * per_sm);
-  kp.batch = batch;
-  int tm_used = 0;
-  if constexpr (KIND == KIND_CHIRP && G::NT > 1 &&
-                TmemCfg<Real, G::NT * G::TPB, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>::OK) {
-    using TMC = TmemCfg<Real, G::NT * G::TPB, G::R, Fft<Real, P, G::NT, ASX_TWTAB_MAX, true>::TSEED_COLS>;
-    using LT = PersistLayout<Real, P, G::NT, G::TPB, true, 1, DBUF>;
-    if (env.use_tmem && per_sm * TMC::NCOLS <= 512 && 2 * kp.m <= P &&
-        LT::total(row_bytes, kp.staged != 0, kp.tw_elems) <= smem) {
-      auto kern_tm = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, true>;
-      static thread_local int tm_attr_for = -1;
-      if (tm_attr_for != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern_tm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)env.smem_optin);
-        if (e != cudaSuccess) return e;
-        tm_attr_for = dev;
-      }
-      kern_tm<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
-      tm_used = 1;
-    }
-  }
-  if (!tm_used) kern<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
-  g_last_launch.tmem = tm_used;
-  g_last_launch.grid = (int)grid;
-  g_last_launch.block = G::NT * G::TPB;
-  g_last_launch.smem = (int)smem;
-  g_last_launch.staged = kp.staged;
-  return cudaGetLastError();
-}
-
-template <typename Real>
-cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t batch, cudaStream_t st,
-                           const LaunchEnv& env) {
-  switch (P) {
-#define ASX_CASE(S)                                                               \
-  case S:                                                                         \
-    return which == ASX_FFT ? launch_persist<Real, S, KIND_AFFT>(kp, batch, st, env) \
-                            : launch_persist<Real, S, KIND_CHIRP>(kp, batch, st, env);
-    ASX_CASE(1)
-    ASX_CASE(2)
-    ASX_CASE(4)
-    ASX_CASE(8)
-    ASX_CASE(16)
-    ASX_CASE(32)
-    ASX_CASE(64)
-    ASX_CASE(128)
-    ASX_CASE(256)
-    ASX_CASE(512)
-    ASX_CASE(1024)
-    ASX_CASE(2048)
-    ASX_CASE(4096)
-    ASX_CASE(8192)
-#undef ASX_CASE
-    case 16384:
-      if constexpr (sizeof(Real) == 4)
-        return which == ASX_FFT ? launch_persist<Real, 16384, KIND_AFFT>(kp, batch, st, env)
-                                : launch_persist<Real, 16384, KIND_CHIRP>(kp, batch, st, env);
-      return cudaErrorInvalidValue;
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
-template <typename Real, int P1>
-cudaError_t launch_cols(int mode, const LParams& lp, cudaStream_t st) {
-  using G = ColCfg<Real, P1>;
-  const unsigned grid = (unsigned)(lp.P2 / kColTile);
-  cudaError_t e = cudaSuccess;
-  auto go = [&](auto kern) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-    if (e == cudaSuccess) kern<<<grid, G::NT * kColTile, G::SMEM, st>>>(lp);
-  };
-  if (mode == COL_FWD_SIGNAL)
-    go(k_large_cols<Real, P1, G::NT, COL_FWD_SIGNAL>);
-  else if (mode == COL_FWD_TABLE)
-    go(k_large_cols<Real, P1, G::NT, COL_FWD_TABLE>);
-  else
-    go(k_large_cols<Real, P1, G::NT, COL_INV_OUT>);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
-}
-
-template <typename Real>
-cudaError_t launch_cols_p1(int64_t P1, int mode, const LParams& lp, cudaStream_t st) {
-  switch (P1) {
-#define ASX_COL(S) \
-  case S:          \
-    return launch_cols<Real, S>(mode, lp, st);
-    ASX_COL(2)
-    ASX_COL(4)
-    ASX_COL(8)
-    ASX_COL(16)
-    ASX_COL(32)
-    ASX_COL(64)
-    ASX_COL(128)
-    ASX_COL(256)
-    ASX_COL(512)
-    ASX_COL(1024)
-#undef ASX_COL
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
-template <typename Real>
-cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st) {
-  constexpr int P2 = sizeof(Real) == 4 ? 16384 : 8192;
-  using G = Cfg<P2, Real>;
-  using E = Fft<Real, P2, G::NT>;
-  const size_t smem = size_t(E::SMEM_ELEMS + E::TAB_ELEMS + 2) * sizeof(typename CT<Real>::T) + 16;
-  cudaError_t e = cudaSuccess;
-  auto go = [&](auto kern) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) kern<<<(unsigned)P1, G::NT, smem, st>>>(lp);
-  };
-  if (mode == ROW_SPECTRUM)
-    go(k_large_rows<Real, P2, G::NT, ROW_SPECTRUM>);
-  else
-    go(k_large_rows<Real, P2, G::NT, ROW_MAIN>);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_large(int dbl, int64_t P1, int mode_cols, int mode_rows, int which, const LParams& lp,
-                         cudaStream_t st) {
-  // which: 0 = cols, 1 = rows
-  if (which == 0) return dbl ? launch_cols_p1<double>(P1, mode_cols, lp, st) : launch_cols_p1<float>(P1, mode_cols, lp, st);
-  return dbl ? launch_rows<double>(mode_rows, P1, lp, st) : launch_rows<float>(mode_rows, P1, lp, st);
-}
-
-template <typename Real, int Q, int NT>
-auto chirp2h_kernel() {
-  return k_chirp2h<Real, Q, NT>;
-}
-
-// Resident CTAs per SM of the two-halves kernel for this precision (0 if n/a).
-int chirp2h_occupancy(int dbl) {
-  int v = 0;
-  if (dbl) {
-    auto k = chirp2h_kernel<double, 4096, 512>();
-    using G = Chirp2hCfg<double, 4096, 512>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 512, G::SMEM) != cudaSuccess)
-      v = 0;
-  } else {
-    auto k = chirp2h_kernel<float, 8192, 512>();
-    using G = Chirp2hCfg<float, 8192, 512>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess ||
-        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, 512, G::SMEM) != cudaSuccess)
-      v = 0;
-  }
-  cudaGetLastError();
-  if (const char* f = std::getenv("ASX_2H_PER_SM")) v = std::atoi(f);  // tuning override
-  return v;
-}
-
-cudaError_t launch_chirp2h(int dbl, const KParams& kp, int grid, void* scratch, const void* cw, const void* cwc,
-                           cudaStream_t st) {
-  if (dbl) {
-    using G = Chirp2hCfg<double, 4096, 512>;
-    k_chirp2h<double, 4096, 512><<<grid, 512, G::SMEM, st>>>(kp, scratch, cw, cwc);
-  } else {
-    using G = Chirp2hCfg<float, 8192, 512>;
-    k_chirp2h<float, 8192, 512><<<grid, 512, G::SMEM, st>>>(kp, scratch, cw, cwc);
-  }
-  g_last_launch.grid = grid;
-  g_last_launch.block = 512;
-  g_last_launch.smem = (int)(dbl ? Chirp2hCfg<double, 4096, 512>::SMEM : Chirp2hCfg<float, 8192, 512>::SMEM);
-  g_last_launch.staged = 4;  // bit 2: two-halves kernel
-  g_last_launch.tmem = 1;
-  return cudaGetLastError();
-}
-
 int two_level_lf(int64_t L) { return (log2i(L) + 1) / 2; }
 
 // Builds [fine(F) | coarse(ceil(L/F))] for W_L at dst.

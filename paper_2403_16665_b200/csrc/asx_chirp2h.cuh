@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NT, 2) k_chirp2h(KParams p, void* scratch_base
 
 // chirpW[k] = W_P^k chirp[k] (k < n), chirpWc[k] = conj(W_P^k) chirp[k] (k < m),
 // evaluated in FP64 from the exactly reduced phases.
-__global__ void k_fill_chirp_tw(void* cw, void* cwc, int64_t n, int64_t m, uint64_t a, uint64_t L2, uint64_t P,
+static __global__ void k_fill_chirp_tw(void* cw, void* cwc, int64_t n, int64_t m, uint64_t a, uint64_t L2, uint64_t P,
                                 int dbl) {
   const int64_t cnt = n > m ? n : m;
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < cnt; k += int64_t(gridDim.x) * blockDim.x) {

@@ -451,7 +451,7 @@ __device__ __forceinline__ void store_c(void* out, int64_t i, double re, double 
 }
 
 // out[k] = W_L^{(k*step) mod L} = exp(-2*pi*i*((k*step) mod L)/L), k < count.
-__global__ void k_fill_roots(void* out, int64_t count, uint64_t step, uint64_t L, int dbl) {
+static __global__ void k_fill_roots(void* out, int64_t count, uint64_t step, uint64_t L, int dbl) {
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count;
        k += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t j = mulmod((uint64_t)k, step, L);
@@ -462,7 +462,7 @@ __global__ void k_fill_roots(void* out, int64_t count, uint64_t step, uint64_t L
 }
 
 // out[k] = exp(-pi*i*((a*k^2) mod L2)/(L2/2)), L2 = 2*d*N.
-__global__ void k_fill_chirp(void* out, int64_t count, uint64_t a, uint64_t L2, int dbl) {
+static __global__ void k_fill_chirp(void* out, int64_t count, uint64_t a, uint64_t L2, int dbl) {
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < count;
        k += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t kk = mulmod((uint64_t)k, (uint64_t)k, L2);
@@ -476,7 +476,7 @@ __global__ void k_fill_chirp(void* out, int64_t count, uint64_t a, uint64_t L2, 
 // H[k] = (1/P) sum_j h[j] W_P^{jk}, h[j] = conj(chirp[j]) (j < M),
 // conj(chirp[P-j]) (P-j < N), else 0.  Direct O(P^2) summation in FP64 with
 // an exact W_P table (plan-time only).
-__global__ void k_chirp_spectrum(void* out, int P, int64_t n, int64_t m, uint64_t a, uint64_t L2,
+static __global__ void k_chirp_spectrum(void* out, int P, int64_t n, int64_t m, uint64_t a, uint64_t L2,
                                  const double2* __restrict__ wP, int dbl) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= P) return;
@@ -502,7 +502,7 @@ __global__ void k_chirp_spectrum(void* out, int P, int64_t n, int64_t m, uint64_
 }
 
 // W[r, c] = W_L^{(a*r*c) mod L}, L = d*n, row-major rows x n.
-__global__ void k_dft_matrix(void* out, int64_t rows, int64_t n, uint64_t a, uint64_t L, int dbl) {
+static __global__ void k_dft_matrix(void* out, int64_t rows, int64_t n, uint64_t a, uint64_t L, int dbl) {
   const int64_t total = rows * n;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -517,7 +517,7 @@ __global__ void k_dft_matrix(void* out, int64_t rows, int64_t n, uint64_t a, uin
 // ------------------------- reference building blocks -----------------------
 
 template <typename Real>
-__global__ void k_combine(const void* y, const void* z, const void* tw, void* out, int64_t rows,
+static __global__ void k_combine(const void* y, const void* z, const void* tw, void* out, int64_t rows,
                           int64_t half) {
   using C = typename CT<Real>::T;
   const C* Y = reinterpret_cast<const C*>(y);
@@ -536,7 +536,7 @@ __global__ void k_combine(const void* y, const void* z, const void* tw, void* ou
 }
 
 template <typename Real>
-__global__ void k_block_sum(const void* x, void* out, int64_t rows, int64_t len) {
+static __global__ void k_block_sum(const void* x, void* out, int64_t rows, int64_t len) {
   using C = typename CT<Real>::T;
   const C* Xp = reinterpret_cast<const C*>(x);
   C* O = reinterpret_cast<C*>(out);

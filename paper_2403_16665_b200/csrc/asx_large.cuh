@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
 
 // h[j] = conj(chirp[j]) (j < M), conj(chirp[P-j]) (P-j < N), else 0.
 template <typename Real>
-__global__ void k_fill_h(void* h, const void* chirp, int64_t P, int64_t n, int64_t m) {
+static __global__ void k_fill_h(void* h, const void* chirp, int64_t P, int64_t n, int64_t m) {
   using C = typename CT<Real>::T;
   for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < P; j += int64_t(gridDim.x) * blockDim.x) {
     C v = mk(Real(0), Real(0));
