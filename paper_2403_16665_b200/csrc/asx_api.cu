@@ -13,6 +13,8 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/asx.h"
 #include "asx_dispatch.cuh"
@@ -96,6 +98,13 @@ struct asx_plan_s {
   LaunchEnv env;
   // execute_host resources
   std::mutex host_mtx;
+  // four-step workspace per stream: the plan's own buffer serves the first
+  // stream that executes, further streams get their own (asx_execute stays
+  // reentrant across streams, including the host path's stream ring)
+  std::mutex ws_mtx;
+  cudaStream_t ws_owner = nullptr;
+  bool ws_owned = false;
+  std::vector<std::pair<cudaStream_t, void*>> ws_extra;
   static constexpr int kLanes = 3;
   cudaStream_t lane[kLanes] = {nullptr, nullptr, nullptr};
   void* din[kLanes] = {nullptr, nullptr, nullptr};
@@ -181,7 +190,26 @@ void fill_kparams(const asx_plan_s* p, KParams& kp) {
   kp.chirp_len = std::max(p->n, p->m);
 }
 
-int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs, int64_t batch,
+void* large_workspace(asx_plan_s* p, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(p->ws_mtx);
+  void* own = static_cast<char*>(p->tables) + p->off_A;
+  if (!p->ws_owned || p->ws_owner == st) {
+    p->ws_owned = true;
+    p->ws_owner = st;
+    return own;
+  }
+  for (auto& kv : p->ws_extra)
+    if (kv.first == st) return kv.second;
+  void* w = nullptr;
+  if (cudaMalloc(&w, celem(p->dtype) * size_t(p->P)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  p->ws_extra.emplace_back(st, w);
+  return w;
+}
+
+int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs, int64_t batch,
                    cudaStream_t st) {
   if (batch == 0 || p->m == 0) return ASX_OK;
   if (batch > 0x7fffffffLL) return fail(ASX_ERR_INVALID, "batch must be < 2^31 per call");
@@ -231,7 +259,8 @@ int launch_execute(const asx_plan_s* p, const void* x, int64_t xs, void* X, int6
     lp.n = p->n;
     lp.m = p->m;
     lp.chirp = base + p->off_chirp;
-    lp.A = base + p->off_A;
+    lp.A = large_workspace(p, st);
+    if (!lp.A) return fail(ASX_ERR_OOM, "four-step workspace allocation failed");
     lp.Ht = base + p->off_H;
     lp.twP1 = base + p->off_twP1;
     lp.twP2 = base + p->off_twP;
@@ -582,6 +611,7 @@ int asx_plan_destroy(asx_plan_t p) {
       if (p->din[i]) cudaFree(p->din[i]);
       if (p->dout[i]) cudaFree(p->dout[i]);
     }
+    for (auto& kv : p->ws_extra) cudaFree(kv.second);
     if (p->tables) cudaFree(p->tables);
   }
   delete p;
