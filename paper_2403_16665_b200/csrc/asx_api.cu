@@ -577,10 +577,12 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
         if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_SPECTRUM, 1, lp, st);
         cudaFreeAsync(hbuf, st);
       }
-    } else if ((e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), sizeof(double2) * p->P, st)) == cudaSuccess) {
+    } else if ((e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), 2 * sizeof(double2) * p->P, st)) ==
+               cudaSuccess) {
+      double2* h_d = wP_d + p->P;
       k_fill_roots<<<(p->P + 255) / 256, 256, 0, st>>>(wP_d, p->P, 1, (uint64_t)p->P, 1);
-      k_chirp_spectrum<<<(p->P + 127) / 128, 128, 0, st>>>(base + p->off_H, p->P, n, m, (uint64_t)a, L2, wP_d,
-                                                           dbl);
+      k_chirp_kernel_fp64<<<(p->P + 255) / 256, 256, 0, st>>>(h_d, p->P, n, m, (uint64_t)a, L2);
+      k_chirp_spectrum<<<(p->P + 127) / 128, 128, 0, st>>>(base + p->off_H, p->P, h_d, wP_d, dbl);
       cudaFreeAsync(wP_d, st);
     }
   }

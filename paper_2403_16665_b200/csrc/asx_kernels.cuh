@@ -476,27 +476,35 @@ static __global__ void k_fill_chirp(void* out, int64_t count, uint64_t a, uint64
 // H[k] = (1/P) sum_j h[j] W_P^{jk}, h[j] = conj(chirp[j]) (j < M),
 // conj(chirp[P-j]) (P-j < N), else 0.  Direct O(P^2) summation in FP64 with
 // an exact W_P table (plan-time only).
-static __global__ void k_chirp_spectrum(void* out, int P, int64_t n, int64_t m, uint64_t a, uint64_t L2,
-                                 const double2* __restrict__ wP, int dbl) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= P) return;
-  double accx = 0.0, accy = 0.0;
-  for (int j = 0; j < P; ++j) {
-    int64_t src;
+static __global__ void k_chirp_kernel_fp64(double2* h, int P, int64_t n, int64_t m, uint64_t a, uint64_t L2) {
+  // h[j] = conj(chirp[j]) (j < M), conj(chirp[P-j]) (P-j < N), else 0, in FP64
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P; j += gridDim.x * blockDim.x) {
+    int64_t src = -1;
     if (j < m)
       src = j;
     else if (P - j < n)
       src = P - j;
-    else
-      continue;
-    const uint64_t kk = mulmod((uint64_t)src, (uint64_t)src, L2);
-    const uint64_t jj = mulmod(kk, a, L2);
-    double s, c;
-    sincospi(2.0 * (double)jj / (double)L2, &s, &c);
-    // h = conj(chirp) = (c, +s)
+    double s = 0.0, c = 0.0;
+    if (src >= 0) {
+      const uint64_t jj = mulmod(mulmod((uint64_t)src, (uint64_t)src, L2), a, L2);
+      sincospi(2.0 * (double)jj / (double)L2, &s, &c);
+    }
+    h[j] = make_double2(c, s);
+  }
+}
+
+// H[k] = (1/P) sum_j h[j] W_P^{jk}: direct FP64 summation against the exact
+// W_P table (plan time only; the table and h stay in L1/L2).
+static __global__ void k_chirp_spectrum(void* out, int P, const double2* __restrict__ h,
+                                        const double2* __restrict__ wP, int dbl) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P) return;
+  double accx = 0.0, accy = 0.0;
+  for (int j = 0; j < P; ++j) {
+    const double2 hv = __ldg(h + j);
     const double2 w = __ldg(wP + (((uint64_t)j * (uint64_t)k) & (uint64_t)(P - 1)));
-    accx += c * w.x - s * w.y;
-    accy += c * w.y + s * w.x;
+    accx += hv.x * w.x - hv.y * w.y;
+    accy += hv.x * w.y + hv.y * w.x;
   }
   store_c(out, k, accx / P, accy / P, dbl);
 }
