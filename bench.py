@@ -63,6 +63,16 @@ def measured_peaks():
         return FALLBACK_HBM_GBS, "fallback"
 
 
+def fp_peak(dtype: str):
+    """Measured FFMA / DFMA peak (TFLOP/s) of a pool B200 (scripts/fp_peaks.cu -> profiles/fp_peaks.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "fp_peaks.json")) as fh:
+            d = json.load(fh)
+        return float(d["fp32_tflops" if dtype == "complex64" else "fp64_tflops"]), "measured (profiles/fp_peaks.json)"
+    except Exception:
+        return (74.4 if dtype == "complex64" else 37.2), "nominal 148 SMs x 1.965 GHz"
+
+
 def profiled_traffic(config_key: str, method: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
     path = os.path.join(REPO, "profiles", "traffic.json")
@@ -234,6 +244,7 @@ def run_gpu(args):
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / avg launch duration
     avg_launch_s = (tot_ms / args.steps) / 1e3
     peak, peak_kind = measured_peaks()
+    fpk, fpk_src = fp_peak(w.dtype)
     achieved = bytes_step / avg_launch_s / 1e9
     flops = w.flops_alg(nloc)
 
@@ -322,7 +333,15 @@ def run_gpu(args):
                 else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "bytes_alg_per_launch": bytes_step,
                 "flops_alg_per_launch": flops, "achieved_alg_tflops": flops / avg_launch_s / 1e12,
-                "kernel": {"fft": "k_afft", "chirp": "k_chirp", "direct": "k_direct"}[plan.method],
+                "kernel": {"fft": "k_fft_persist<afft>", "chirp": "k_fft_persist<chirp>",
+                           "direct": "k_direct"}[plan.method],
+                # the FP-side roofline of the same launches (configs 1b-4 are FP-bound)
+                "compute": {"pipe": "fp32" if w.dtype == "complex64" else "fp64",
+                            "achieved_tflops": flops / avg_launch_s / 1e12, "peak_tflops": fpk,
+                            "frac": flops / avg_launch_s / 1e12 / fpk, "peak_source": fpk_src,
+                            "flops": "8*M*N per signal (direct form: alpha has no dyadic alpha-FFT count)"
+                            if (w.n * w.alpha.denominator) % w.alpha.numerator
+                            else "reference alpha-FFT op count 6*mults+2*adds per signal (fastpath.py:113-127)"},
             },
             "other_methods": alt,
             "cpu_baseline": cpu,
