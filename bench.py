@@ -73,6 +73,34 @@ def fp_peak(dtype: str):
         return (74.4 if dtype == "complex64" else 37.2), "nominal 148 SMs x 1.965 GHz"
 
 
+def pcie_duplex(dev, mib=256, reps=3):
+    """Concurrent H2D + D2H bandwidth from pinned memory (GB/s per direction): the e2e roofline."""
+    import torch
+
+    n = mib << 20
+    h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d_in = torch.empty(n, dtype=torch.uint8, device=dev)
+    d_out = torch.zeros(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    best_h2d = best_d2h = 0.0
+    for _ in range(reps + 1):
+        torch.cuda.synchronize(dev)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        evs[0].record(s1)
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        evs[1].record(s1)
+        evs[2].record(s2)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+        evs[3].record(s2)
+        torch.cuda.synchronize(dev)
+        best_h2d = max(best_h2d, n / (evs[0].elapsed_time(evs[1]) / 1e3) / 1e9)
+        best_d2h = max(best_d2h, n / (evs[2].elapsed_time(evs[3]) / 1e3) / 1e9)
+    return best_h2d, best_d2h
+
+
 def profiled_traffic(config_key: str, method: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
     path = os.path.join(REPO, "profiles", "traffic.json")
@@ -296,6 +324,12 @@ def run_gpu(args):
         # cross-check the host-path result against the device-path result (untimed)
         same = torch.equal(hX.to(dev), out)
         e2e["matches_device_path"] = bool(same)
+        # e2e roofline: both directions of the PCIe link at once (the ring overlaps them)
+        h2d_gbs, d2h_gbs = pcie_duplex(dev)
+        bound_s = max(e2e["h2d_bytes_per_step"] / (h2d_gbs * 1e9), e2e["d2h_bytes_per_step"] / (d2h_gbs * 1e9))
+        e2e["roofline"] = {"bound": "pcie", "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                           "how": "concurrent pinned 256 MiB copies on two streams, best of 3",
+                           "bound_ms": bound_s * 1e3, "frac": bound_s / e2e_s}
 
     # untimed verification collective: per-rank checksums gathered over NCCL
     checks = gather_checksums(out, device=dev)

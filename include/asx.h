@@ -111,7 +111,9 @@ int asx_execute(asx_plan_t plan, const void* x, int64_t x_stride, void* X,
 
 /* Same transform on HOST buffers (pinned for overlap): the batch is cut into
  * chunks that are copied host->device, transformed and copied back on a
- * small ring of streams so the copies overlap the kernels.  Synchronous:
+ * small ring of streams so the copies overlap the kernels.  chunk = rows
+ * per chunk; chunk <= 0 picks ~128 MiB chunks that ramp up from 1/8 at the
+ * start and down at the end (short pipeline fill and drain).  Synchronous:
  * returns after the last result byte is in X. */
 int asx_execute_host(asx_plan_t plan, const void* x, int64_t x_stride, void* X,
                      int64_t X_stride, int64_t batch, int64_t chunk);

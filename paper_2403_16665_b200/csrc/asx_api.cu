@@ -666,8 +666,29 @@ int asx_execute_host(asx_plan_t p, const void* x, int64_t x_stride, void* X, int
   if (!guard.ok) return fail(ASX_ERR_CUDA, "cannot select CUDA device");
   const size_t ib = in_elem(p), ob = celem(p->dtype);
   const size_t in_row = (size_t)p->n * ib, out_row = (size_t)p->m * ob;
-  if (chunk <= 0) chunk = std::max<int64_t>(1, (int64_t)((64ull << 20) / std::max(in_row + out_row, (size_t)1)));
+  // default: ~128 MiB of in+out per chunk, with chunk sizes ramping up from
+  // 1/8 at the start and back down at the end, so the pipeline fill (first
+  // H2D alone) and drain (last D2H alone) are short while the steady state
+  // amortises the per-copy DMA setup (scripts/e2e_chunks.py)
+  const bool ramp = chunk <= 0;
+  if (ramp) chunk = std::max<int64_t>(1, (int64_t)((128ull << 20) / std::max(in_row + out_row, (size_t)1)));
   chunk = std::min(chunk, batch);
+  std::vector<int64_t> sizes;
+  {
+    int64_t left = batch;
+    if (ramp)
+      for (int64_t s = std::max<int64_t>(1, chunk / 8); s < chunk && left > 0; s *= 2) {
+        sizes.push_back(std::min(s, left));
+        left -= sizes.back();
+      }
+    const int64_t smin = ramp ? std::max<int64_t>(1, chunk / 8) : chunk;
+    while (left > 0) {
+      int64_t s = chunk;
+      if (ramp && left < 2 * chunk) s = std::max(smin, (left + 1) / 2);
+      sizes.push_back(std::min(s, left));
+      left -= sizes.back();
+    }
+  }
   if (chunk > p->lane_rows) {
     for (int i = 0; i < asx_plan_s::kLanes; ++i) {
       if (p->din[i]) cudaFree(p->din[i]);
@@ -683,8 +704,9 @@ int asx_execute_host(asx_plan_t p, const void* x, int64_t x_stride, void* X, int
     p->lane_rows = chunk;
   }
   int k = 0;
-  for (int64_t b0 = 0; b0 < batch; b0 += chunk, k = (k + 1) % asx_plan_s::kLanes) {
-    const int64_t rows = std::min(chunk, batch - b0);
+  int64_t b0 = 0;
+  for (size_t c = 0; c < sizes.size(); b0 += sizes[c], ++c, k = (k + 1) % asx_plan_s::kLanes) {
+    const int64_t rows = sizes[c];
     cudaStream_t st = p->lane[k];
     const char* src = static_cast<const char*>(x) + (size_t)b0 * x_stride * ib;
     char* dst = static_cast<char*>(X) + (size_t)b0 * X_stride * ob;

@@ -10,7 +10,7 @@ x = generate_device(w, 0, B, device="cuda")
 hx = torch.empty(x.shape, dtype=x.dtype, pin_memory=True); hx.copy_(x)
 hX = torch.empty((B, w.m), dtype=x.dtype, pin_memory=True)
 p = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype)
-for rows in (128, 256, 512, 1024, 2048):
+for rows in [int(r) for r in (sys.argv[2].split(",") if len(sys.argv) > 2 else (0, 128, 256, 512, 1024, 2048))]:
     p.execute_host(hx.numpy(), out=hX.numpy(), chunk=rows)
     t0 = time.perf_counter()
     for _ in range(3):
