@@ -1,6 +1,7 @@
 #!/bin/bash
-# Official measurement set: bench line, ncu launch list and full capture of the
-# bench's dominant kernel (same command line), GPU parity tests, smoke.
+# Official measurement set: GPU parity tests, smoke, bench line (both arms) and
+# the ncu launch list of the bench command (one ncu per gpurun call: the full
+# capture of the dominant kernel is scripts/gpu_ncu_full.sh, a separate call).
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 TAG=${TAG:-r1}
@@ -11,6 +12,4 @@ timeout 600 python bench.py --impl reference --steps 1 > gpurun_out/bench_ref_$T
 CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alt"
 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
-$CMD > gpurun_out/plain2_$TAG.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fft_persist -s 3 -c 1 -o gpurun_out/prof_bench_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo done
