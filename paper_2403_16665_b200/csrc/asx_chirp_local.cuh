@@ -1,0 +1,346 @@
+// asx_chirp_local.cuh — chirp-z convolution for P = 16384 (complex64) with
+// group-local exchanges: the config-4 hot kernel (BASELINE config 4:
+// N = M = 8192, α = 1/8).
+//
+// Same mathematics as k_fft_persist<KIND_CHIRP> (the α-DFT as the chirp-z
+// convolution X_m = c_m Σ_n (x_n c_n) conj(c_{m-n}), fastpath.py:162-181 /
+// oracle.py:50-67 restated), but the P-point forward FFT is decimation in
+// FREQUENCY and the inverse its exact transpose (decimation in time on the
+// digit-reversed spectrum), so the spectrum is never reordered and most data
+// exchanges stay inside small thread groups:
+//
+//   P1  radix-16 DIF over x[t + 1024 i] (the io layout, no exchange), twiddle
+//       W_16384^{t k1}                          -> 16 sub-problems of 1024
+//   G1  global exchange (CTA barrier): sub-problem k1 -> threads 64 k1 ..
+//   P2  radix-4 DIF (4 groups/thread), twiddle W_1024^{n' k2} (exact table)
+//   L1  exchange inside the 2-warp group (named barrier)
+//   P3  radix-16 DIF, twiddle W_256^{n'' k3}    -> 16-point sub-problems
+//   L2  exchange inside the half-warp (__syncwarp)
+//   P4  radix-16 DIF, no twiddle                -> Y[f], f = k1 + 16 k2 + 64 k3 + 1024 k4
+//   × H[f] (tensor memory, stored in this per-thread order), conj
+//   Q1..Q4 = P4ᵀ..P1ᵀ on the same thread/data mapping (twiddle, then butterfly,
+//   then the inverse exchange), ending in the io layout: X[t + 1024 i].
+//
+// Per signal: 2 CTA-wide exchanges instead of 6, 2 group-local, 2 warp-local;
+// warps drift apart inside the local phases so butterflies (FP32 pipe) and
+// exchanges (shared-memory pipe) of different groups overlap.
+#pragma once
+
+#include "asx_kernels.cuh"
+
+#ifndef ASX_CL_P3TAB
+#define ASX_CL_P3TAB 1  // P3/Q2 twiddles from the full exact [15][16] table (else exact seeds + chain)
+#endif
+#ifndef ASX_CL_P1EXACT
+#define ASX_CL_P1EXACT 1  // P1/Q4 twiddles w, w^2, w^3 exact from TMEM (else w^2, w^3 by products)
+#endif
+
+namespace asx {
+
+struct ChirpLocal {
+  static constexpr int P = 16384, NT = 1024, R = 16;
+  static constexpr int SUB = 272;       // one 256-element sub-block (+16 pad: L2's 17-stride rows fit)
+  static constexpr int REG = 4 * SUB;   // one 1024-point sub-problem
+  static constexpr int XB = 16 * REG;   // exchange buffer (complex elements)
+  static constexpr int T2N = 3 * 256;   // W_1024^{n' k2}, k2 = 1..3, n' < 256
+  static constexpr int T3N = 15 * 16;   // W_256^{n'' k3}, k3 = 1..15, n'' < 16 (exact; [0..2] = seeds W^{4a n''} w/o ASX_CL_P3TAB)
+  static constexpr int CPT = 64;        // TMEM columns per thread: H 32 | chirp 16 | P1 twiddles 16
+  // position of element n (< 1024) of a sub-problem inside its region
+  __host__ __device__ static constexpr int pos(int n) { return n + (n >> 8) * (SUB - 256); }
+  template <typename C>
+  __host__ __device__ static size_t stage_off() { return align_up(size_t(XB) * sizeof(C), 128); }
+  template <typename C>
+  __host__ __device__ static size_t tab_off(size_t row_bytes, bool staged) {
+    return stage_off<C>() + (staged ? align_up(row_bytes, 128) : 0);
+  }
+  template <typename C>
+  __host__ __device__ static size_t bar_off(size_t row_bytes, bool staged) {
+    return align_up(tab_off<C>(row_bytes, staged) + size_t(T2N + T3N) * sizeof(C), 16);
+  }
+  template <typename C>
+  __host__ __device__ static size_t total(size_t row_bytes, bool staged) {
+    return bar_off<C>(row_bytes, staged) + 2 * sizeof(uint64_t) + 16;  // stage mbar, WAR mbar, TMEM slot
+  }
+};
+
+template <typename C>
+__device__ __forceinline__ C exact_w(int e, int L) {  // W_L^e rounded once from FP64
+  double sn, cs;
+  sincospi(2.0 * double(e) / double(L), &sn, &cs);
+  using Rl = decltype(C{}.x);
+  return mk(Rl(cs), Rl(-sn));
+}
+
+// u[r] *= w^r (r < 16) from exact w, w^2, w^3 and exact seeds w^{4a}
+// (w = {w1, w2, w3, s1, s2, s3, -, -}): every applied twiddle is at most one
+// product of exact values.
+template <typename C>
+__device__ __forceinline__ void tw16_apply(C (&u)[16], const C (&w)[8]) {
+  u[1] = cmul(u[1], w[0]);
+  u[2] = cmul(u[2], w[1]);
+  u[3] = cmul(u[3], w[2]);
+#pragma unroll
+  for (int a = 1; a < 4; ++a) {
+    const C w4a = w[2 + a];
+    u[4 * a] = cmul(u[4 * a], w4a);
+    u[4 * a + 1] = cmul(u[4 * a + 1], cmul(w4a, w[0]));
+    u[4 * a + 2] = cmul(u[4 * a + 2], cmul(w4a, w[1]));
+    u[4 * a + 3] = cmul(u[4 * a + 3], cmul(w4a, w[2]));
+  }
+}
+
+__device__ __forceinline__ void group_bar(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
+  using C = typename CT<Real>::T;
+  using L = ChirpLocal;
+  static_assert(sizeof(C) == 8, "TMEM column layout assumes complex64");
+  constexpr int WPC = 2, CPC = 4;  // words per complex, complex per 8-column TMEM access
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* xb = reinterpret_cast<C*>(smraw);
+  const int t = threadIdx.x, warp = t >> 5;
+  const int gk = t >> 6;           // P2/Q3: sub-problem k1 of this thread's group
+  const int tau = t & 63;          // P2/Q3: n' = tau + 64 g
+  const int k2 = tau >> 4;         // P3..Q2: sub-block
+  const int n16 = t & 15;          // P3/Q2: n''; P4/Q1: k3
+  const int gbar = 1 + (t >> 7);   // named barrier of this 4-warp pair of groups
+  const bool staged = p.staged != 0;
+  const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(Real) : sizeof(C));
+  unsigned char* stage = smraw + L::stage_off<C>();
+  C* T2 = reinterpret_cast<C*>(smraw + L::tab_off<C>(row_bytes, staged));
+  C* T3 = T2 + L::T2N;
+  uint64_t* stbar = reinterpret_cast<uint64_t*>(smraw + L::bar_off<C>(row_bytes, staged));
+  uint64_t* war = stbar + 1;
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(stbar + 2);
+
+  for (int e = t; e < L::T2N; e += L::NT) T2[e] = exact_w<C>((e & 255) * (e / 256 + 1), 1024);
+  for (int e = t; e < L::T3N; e += L::NT)
+    T3[e] = exact_w<C>((ASX_CL_P3TAB ? (e / 16 + 1) : (e < 48 ? 4 * (e / 16 + 1) : 0)) * (e & 15), 256);
+  const C w1c = exact_w<C>(n16, 256);  // P3 / Q2 base twiddle W_256^{n''} (chain variant)
+  if (t == 0) {
+    mbar_init(stbar, 1);
+    mbar_init(war, L::NT / 32);
+    fence_mbar_init();
+  }
+  const int stride = int(gridDim.x);
+  int u = int(blockIdx.x);
+  const int batch = int(p.batch);
+  const int iters = (batch + stride - 1) / stride;
+  const C* chirp = reinterpret_cast<const C*>(p.chirp);
+  const C* H = reinterpret_cast<const C*>(p.H);
+
+  // tensor memory: H in this thread's spectrum order, the chirp, P1 seeds
+  if (warp == 0) tmem_alloc(&tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * L::CPT);
+  {
+    const int fbase = gk + 16 * k2 + 64 * n16;  // f = fbase + 1024 k4
+#pragma unroll
+    for (int j0 = 0; j0 < 16; j0 += CPC) {
+      uint32_t wh[8], wc[8];
+#pragma unroll
+      for (int k = 0; k < CPC; ++k) {
+        c_to_words(__ldg(H + fbase + 1024 * (j0 + k)), &wh[k * WPC]);
+        const int idx = t + 1024 * (j0 + k);
+        c_to_words((j0 + k < 8 && idx < p.chirp_len) ? __ldg(chirp + idx) : mk(Real(0), Real(0)), &wc[k * WPC]);
+      }
+      tmem_st8(tbase + j0 * WPC, wh);
+      if (j0 < 8) tmem_st8(tbase + 32 + j0 * WPC, wc);
+    }
+    // P1 / Q4 twiddles of W = W_16384^t: {W, W^2, W^3, W^4, W^8, W^12} (exact)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t ws[8];
+#pragma unroll
+      for (int k = 0; k < CPC; ++k) {
+        const int i = 4 * h + k;
+        const int e = i < 3 ? (i + 1) * t : (i < 6 ? 4 * (i - 2) * t : 0);
+        c_to_words(exact_w<C>(e & (L::P - 1), L::P), &ws[k * WPC]);
+      }
+      tmem_st8(tbase + 48 + 8 * h, ws);
+    }
+    tmem_wait_st();
+  }
+  __syncthreads();
+  if (staged && t == 0 && u < batch) {
+    mbar_expect_tx(stbar, (uint32_t)row_bytes);
+    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * (row_bytes / p.n),
+                (uint32_t)row_bytes, stbar);
+  }
+  uint32_t phase = 0, xcnt = 0;
+  auto ld_tm = [&](int col, C (&out)[CPC]) {
+    uint32_t w[8];
+    tmem_ld8(tbase + col, w);
+#pragma unroll
+    for (int k = 0; k < CPC; ++k) out[k] = words_to_c(&w[k * WPC], (C*)nullptr);
+  };
+  auto tw_p1 = [&](C (&w)[8]) {
+    ld_tm(48, reinterpret_cast<C(&)[CPC]>(w[0]));
+    ld_tm(56, reinterpret_cast<C(&)[CPC]>(w[4]));
+    if (!ASX_CL_P1EXACT) {
+      w[1] = cmul(w[0], w[0]);
+      w[2] = cmul(w[1], w[0]);
+    }
+  };
+  // P3 / Q2: u[k3] *= W_256^{n'' k3} from the exact shared table (or chains)
+  auto tw_p3 = [&](C (&u3)[16]) {
+    if (ASX_CL_P3TAB) {
+#pragma unroll
+      for (int r = 1; r < 16; ++r) u3[r] = cmul(u3[r], T3[(r - 1) * 16 + n16]);
+    } else {
+      C w[8];
+      w[0] = w1c;
+      w[1] = cmul(w1c, w1c);
+      w[2] = cmul(w[1], w1c);
+      w[3] = T3[n16];
+      w[4] = T3[16 + n16];
+      w[5] = T3[32 + n16];
+      tw16_apply(u3, w);
+    }
+  };
+  C* const rg = xb + gk * L::REG;             // this group's region
+  C* const sb = rg + k2 * L::SUB;             // this half-warp's sub-block
+
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it, u += stride) {
+    const bool live = u < batch;
+    const int64_t row_off = int64_t(u) * p.xs;
+    C v[16];
+    if (staged && live) {
+      mbar_wait(stbar, phase);
+      phase ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = mk(Real(0), Real(0));
+#pragma unroll
+    for (int j0 = 0; j0 < 8; j0 += CPC) {
+      C cw[CPC];
+      ld_tm(32 + j0 * WPC, cw);
+#pragma unroll
+      for (int k = 0; k < CPC; ++k) {
+        const int nn = t + 1024 * (j0 + k);
+        if (live && nn < p.n) v[j0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+      }
+    }
+    // ---- P1: radix-16 DIF over x[t + 1024 i] (upper half zero), twiddle W_16384^{t k1}
+    dft_reg<16>(v);
+    {
+      C w[8];
+      tw_p1(w);
+      tw16_apply(v, w);
+    }
+    // ---- G1: y_k1[t] -> region k1 (WAR: previous signal's Q4 reads)
+    if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) xb[k1 * L::REG + L::pos(t)] = v[k1];
+    __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
+    if (staged && t == 0 && u + stride < batch) {
+      fence_proxy_async();
+      mbar_expect_tx(stbar, (uint32_t)row_bytes);
+      tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * (row_bytes / p.n),
+                  (uint32_t)row_bytes, stbar);
+    }
+    // ---- P2: radix-4 DIF over y_k[n' + 256 i'], n' = tau + 64 g; twiddle W_1024^{n' k2}
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[4 * g + i] = rg[tau + 64 * g + L::SUB * i];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      dft_reg<4>(reinterpret_cast<C(&)[4]>(v[4 * g]));
+#pragma unroll
+      for (int j = 1; j < 4; ++j) v[4 * g + j] = cmul(v[4 * g + j], T2[(j - 1) * 256 + tau + 64 * g]);
+    }
+    // no WAR barrier: each thread overwrites exactly the slots it read
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) rg[j * L::SUB + tau + 64 * g] = v[4 * g + j];
+    group_bar(gbar);  // RAW
+    // ---- P3: radix-16 DIF over z_{k,k2}[n'' + 16 i'']; twiddle W_256^{n'' k3}
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = sb[n16 + 16 * i];
+    dft_reg<16>(v);
+    tw_p3(v);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sb[17 * j + n16] = v[j];
+    __syncwarp();
+    // ---- P4: radix-16 DIF over n'' (no twiddle) -> Y[f], f = gk + 16 k2 + 64 n16 + 1024 k4
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = sb[17 * n16 + i];
+    dft_reg<16>(v);
+#pragma unroll
+    for (int j0 = 0; j0 < 16; j0 += CPC) {
+      C hw[CPC];
+      ld_tm(j0 * WPC, hw);
+#pragma unroll
+      for (int k = 0; k < CPC; ++k) v[j0 + k] = cconj(cmul(v[j0 + k], hw[k]));
+    }
+    // ---- inverse = conj(DFT(conj(.))), DFT as the transposed passes Q1..Q4
+    dft_reg<16>(v);  // Q1 = P4^T
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sb[17 * n16 + i] = v[i];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = sb[17 * j + n16];
+    tw_p3(v);  // Q2 = P3^T
+    dft_reg<16>(v);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sb[n16 + 16 * i] = v[i];
+    group_bar(gbar);  // RAW
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[4 * g + j] = rg[j * L::SUB + tau + 64 * g];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {  // Q3 = P2^T
+#pragma unroll
+      for (int j = 1; j < 4; ++j) v[4 * g + j] = cmul(v[4 * g + j], T2[(j - 1) * 256 + tau + 64 * g]);
+      dft_reg<4>(reinterpret_cast<C(&)[4]>(v[4 * g]));
+    }
+    // no WAR barrier: each thread overwrites exactly the slots it read
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rg[tau + 64 * g + L::SUB * i] = v[4 * g + i];
+    __syncthreads();
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
+    __syncwarp();
+    if ((t & 31) == 0) mbar_arrive(war);
+    ++xcnt;
+    {
+      C w[8];
+      tw_p1(w);
+      tw16_apply(v, w);
+    }
+    dft_reg<16>(v);
+    {
+      C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+#pragma unroll
+      for (int j0 = 0; j0 < 8; j0 += CPC) {
+        C cw[CPC];
+        ld_tm(32 + j0 * WPC, cw);
+#pragma unroll
+        for (int k = 0; k < CPC; ++k) {
+          const int mm = t + 1024 * (j0 + k);
+          if (live && mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(tmem_slot, 512);
+}
+
+}  // namespace asx

@@ -11,6 +11,7 @@
 
 #include "../../include/asx.h"
 #include "asx_chirp2h.cuh"
+#include "asx_chirp_local.cuh"
 #include "asx_large.cuh"
 
 namespace asx_host {
@@ -20,6 +21,7 @@ struct LaunchEnv {
   int sms = 148;
   size_t smem_optin = 227 * 1024;
   int use_tmem = 1;  // chirp tables in tensor memory (env ASX_NO_TMEM=1 disables, for A/B runs)
+  int use_local = 1; // P = 16384 complex64 chirp on k_chirp_local (env ASX_NO_LOCAL=1 disables)
 };
 
 // Shape of the most recent launch on this thread (asx_last_launch, for
@@ -53,6 +55,9 @@ extern thread_local LastLaunch g_last_launch;
 #ifndef ASX_MT_C128
 #define ASX_MT_C128 512  // threads per SM the register budget targets (c128)
 #endif
+#ifndef ASX_MT_C128_SMALL
+#define ASX_MT_C128_SMALL ASX_MT_C128  // the same for c128 P <= 4096
+#endif
 template <int P, typename Real> struct Cfg {
   static constexpr bool DBL = sizeof(Real) == 8;
   static constexpr int R = (P <= 32)     ? P
@@ -61,7 +66,7 @@ template <int P, typename Real> struct Cfg {
                                          : (P == 16384 ? ASX_R_16K_C64 : ASX_R_BIG_C64);
   static constexpr int NT = P / R;
   static constexpr int TPB = (NT == 1) ? 64 : (NT >= 256 ? 1 : 256 / NT);
-  static constexpr int MT = DBL ? ASX_MT_C128 : ASX_MT_C64;
+  static constexpr int MT = DBL ? (P <= 4096 ? ASX_MT_C128_SMALL : ASX_MT_C128) : ASX_MT_C64;
   static constexpr int MINB = (MT / (NT * TPB)) > 1 ? (MT / (NT * TPB)) : 1;
   // α-FFT residues transformed together per thread (ILP for the latency-bound FP64 case)
   static constexpr int KR = (DBL && P == 4096) ? ASX_KR_C128_4K : ((!DBL && P == 8192) ? ASX_KR_C64_8K : 1);
@@ -113,6 +118,35 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
     return c.per_sm;
   };
   if (G::NT == 1) kp.staged = 0;
+  if constexpr (KIND == KIND_CHIRP && sizeof(Real) == 4 && P == ChirpLocal::P) {
+    // group-local exchange kernel (asx_chirp_local.cuh): one CTA per SM
+    if (env.use_local && env.use_tmem && 2 * kp.m <= P && 2 * kp.n <= P && batch < (int64_t(1) << 31)) {
+      using CL = ChirpLocal;
+      auto kl = k_chirp_local<float>;
+      size_t smem_l = CL::total<typename CT<Real>::T>(row_bytes, kp.staged != 0);
+      if (smem_l > env.smem_optin) {
+        kp.staged = 0;
+        smem_l = CL::total<typename CT<Real>::T>(row_bytes, false);
+      }
+      static thread_local int cl_attr_for = -1;
+      int dev_l = 0;
+      cudaGetDevice(&dev_l);
+      if (cl_attr_for != dev_l) {
+        cudaError_t e = cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
+        if (e != cudaSuccess) return e;
+        cl_attr_for = dev_l;
+      }
+      const int64_t grid_l = std::min<int64_t>(batch, env.sms);
+      kp.batch = batch;
+      kl<<<(unsigned)grid_l, CL::NT, smem_l, st>>>(kp);
+      g_last_launch.tmem = 2;
+      g_last_launch.grid = (int)grid_l;
+      g_last_launch.block = CL::NT;
+      g_last_launch.smem = (int)smem_l;
+      g_last_launch.staged = kp.staged;
+      return cudaGetLastError();
+    }
+  }
   const size_t smem_u = L::total(row_bytes, false, kp.tw_elems);
   const int occ_u = occ(0, smem_u);
   size_t smem = smem_u;
