@@ -39,7 +39,8 @@ namespace asx {
 
 struct ChirpLocal {
   static constexpr int P = 16384, NT = 1024, R = 16;
-  static constexpr int SUB = 272;       // one 256-element sub-block (+16 pad: L2's 17-stride rows fit)
+  static constexpr int L2S = 18;        // L2 row stride: 16-byte aligned rows, conflict-free columns
+  static constexpr int SUB = 288;       // one 256-element sub-block (+32 pad: L2's 18-stride rows fit)
   static constexpr int REG = 4 * SUB;   // one 1024-point sub-problem
   static constexpr int XB = 16 * REG;   // exchange buffer (complex elements)
   static constexpr int T2N = 3 * 256;   // W_1024^{n' k2}, k2 = 1..3, n' < 256
@@ -89,6 +90,16 @@ __device__ __forceinline__ void tw16_apply(C (&u)[16], const C (&w)[8]) {
   }
 }
 
+// two adjacent complex64 values as one 16-byte shared-memory access
+__device__ __forceinline__ void ld_pair(const float2* a, float2& x, float2& y) {
+  const float4 w = *reinterpret_cast<const float4*>(a);
+  x = make_float2(w.x, w.y);
+  y = make_float2(w.z, w.w);
+}
+__device__ __forceinline__ void st_pair(float2* a, float2 x, float2 y) {
+  *reinterpret_cast<float4*>(a) = make_float4(x.x, x.y, y.x, y.y);
+}
+
 __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
@@ -103,7 +114,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
   C* xb = reinterpret_cast<C*>(smraw);
   const int t = threadIdx.x, warp = t >> 5;
   const int gk = t >> 6;           // P2/Q3: sub-problem k1 of this thread's group
-  const int tau = t & 63;          // P2/Q3: n' = tau + 64 g
+  const int tau = t & 63;          // P2/Q3: n' = 2 tau + (g & 1) + 128 (g >> 1) (adjacent pairs)
   const int k2 = tau >> 4;         // P3..Q2: sub-block
   const int n16 = t & 15;          // P3/Q2: n''; P4/Q1: k3
   const int gbar = 1 + (t >> 7);   // named barrier of this 4-warp pair of groups
@@ -203,6 +214,19 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       tw16_apply(u3, w);
     }
   };
+  // twiddle tables are prefetched into registers right after an exchange
+  // write (the data registers are free then), i.e. inside the barrier shadow
+  auto ld_t2 = [&](C (&w)[12]) {  // W_1024^{n' k2}, n' = 2 tau + (g & 1) + 128 (g >> 1), k2 = 1..3
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 1; j < 4; ++j)
+        ld_pair(T2 + (j - 1) * 256 + 2 * tau + 128 * h, w[3 * (2 * h) + j - 1], w[3 * (2 * h + 1) + j - 1]);
+  };
+  auto ld_t3 = [&](C (&w)[15]) {  // W_256^{n'' k3}, k3 = 1..15
+#pragma unroll
+    for (int r = 1; r < 16; ++r) w[r - 1] = T3[(r - 1) * 16 + n16];
+  };
   C* const rg = xb + gk * L::REG;             // this group's region
   C* const sb = rg + k2 * L::SUB;             // this half-warp's sub-block
 
@@ -238,6 +262,8 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) xb[k1 * L::REG + L::pos(t)] = v[k1];
+    C tw2[12];
+    ld_t2(tw2);
     __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
     if (staged && t == 0 && u + stride < batch) {
       fence_proxy_async();
@@ -245,22 +271,22 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * (row_bytes / p.n),
                   (uint32_t)row_bytes, stbar);
     }
-    // ---- P2: radix-4 DIF over y_k[n' + 256 i'], n' = tau + 64 g; twiddle W_1024^{n' k2}
+    // ---- P2: radix-4 DIF over y_k[n' + 256 i'], n' = 2 tau + (g & 1) + 128 (g >> 1); twiddle W_1024^{n' k2}
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[4 * g + i] = rg[tau + 64 * g + L::SUB * i];
+      for (int i = 0; i < 4; ++i) ld_pair(rg + 2 * tau + 128 * h + L::SUB * i, v[4 * (2 * h) + i], v[4 * (2 * h + 1) + i]);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       dft_reg<4>(reinterpret_cast<C(&)[4]>(v[4 * g]));
 #pragma unroll
-      for (int j = 1; j < 4; ++j) v[4 * g + j] = cmul(v[4 * g + j], T2[(j - 1) * 256 + tau + 64 * g]);
+      for (int j = 1; j < 4; ++j) v[4 * g + j] = cmul(v[4 * g + j], tw2[3 * g + j - 1]);
     }
     // no WAR barrier: each thread overwrites exactly the slots it read
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) rg[j * L::SUB + tau + 64 * g] = v[4 * g + j];
+      for (int j = 0; j < 4; ++j) st_pair(rg + j * L::SUB + 2 * tau + 128 * h, v[4 * (2 * h) + j], v[4 * (2 * h + 1) + j]);
     group_bar(gbar);  // RAW
     // ---- P3: radix-16 DIF over z_{k,k2}[n'' + 16 i'']; twiddle W_256^{n'' k3}
 #pragma unroll
@@ -269,11 +295,18 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     tw_p3(v);
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sb[17 * j + n16] = v[j];
+    for (int j = 0; j < 16; ++j) sb[L::L2S * j + n16] = v[j];
     __syncwarp();
     // ---- P4: radix-16 DIF over n'' (no twiddle) -> Y[f], f = gk + 16 k2 + 64 n16 + 1024 k4
+    {
+      const float4* row = reinterpret_cast<const float4*>(sb + L::L2S * n16);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = sb[17 * n16 + i];
+      for (int q = 0; q < 8; ++q) {
+        const float4 w = row[q];
+        v[2 * q] = mk(Real(w.x), Real(w.y));
+        v[2 * q + 1] = mk(Real(w.z), Real(w.w));
+      }
+    }
     dft_reg<16>(v);
 #pragma unroll
     for (int j0 = 0; j0 < 16; j0 += CPC) {
@@ -285,43 +318,45 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     // ---- inverse = conj(DFT(conj(.))), DFT as the transposed passes Q1..Q4
     dft_reg<16>(v);  // Q1 = P4^T
     __syncwarp();
+    {
+      float4* row = reinterpret_cast<float4*>(sb + L::L2S * n16);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) sb[17 * n16 + i] = v[i];
+      for (int q = 0; q < 8; ++q) row[q] = make_float4(v[2 * q].x, v[2 * q].y, v[2 * q + 1].x, v[2 * q + 1].y);
+    }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = sb[17 * j + n16];
+    for (int j = 0; j < 16; ++j) v[j] = sb[L::L2S * j + n16];
     tw_p3(v);  // Q2 = P3^T
     dft_reg<16>(v);
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 16; ++i) sb[n16 + 16 * i] = v[i];
+    ld_t2(tw2);
     group_bar(gbar);  // RAW
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[4 * g + j] = rg[j * L::SUB + tau + 64 * g];
+      for (int j = 0; j < 4; ++j) ld_pair(rg + j * L::SUB + 2 * tau + 128 * h, v[4 * (2 * h) + j], v[4 * (2 * h + 1) + j]);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // Q3 = P2^T
 #pragma unroll
-      for (int j = 1; j < 4; ++j) v[4 * g + j] = cmul(v[4 * g + j], T2[(j - 1) * 256 + tau + 64 * g]);
+      for (int j = 1; j < 4; ++j) v[4 * g + j] = cmul(v[4 * g + j], tw2[3 * g + j - 1]);
       dft_reg<4>(reinterpret_cast<C(&)[4]>(v[4 * g]));
     }
     // no WAR barrier: each thread overwrites exactly the slots it read
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) rg[tau + 64 * g + L::SUB * i] = v[4 * g + i];
+      for (int i = 0; i < 4; ++i) st_pair(rg + 2 * tau + 128 * h + L::SUB * i, v[4 * (2 * h) + i], v[4 * (2 * h + 1) + i]);
+    C tw1[8];
+    tw_p1(tw1);
     __syncthreads();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
     __syncwarp();
     if ((t & 31) == 0) mbar_arrive(war);
     ++xcnt;
-    {
-      C w[8];
-      tw_p1(w);
-      tw16_apply(v, w);
-    }
+    tw16_apply(v, tw1);
     dft_reg<16>(v);
     {
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;

@@ -55,8 +55,8 @@ extern thread_local LastLaunch g_last_launch;
 #ifndef ASX_MT_C128
 #define ASX_MT_C128 512  // threads per SM the register budget targets (c128)
 #endif
-#ifndef ASX_MT_C128_SMALL
-#define ASX_MT_C128_SMALL ASX_MT_C128  // the same for c128 P <= 4096
+#ifndef ASX_MT_C128_4K
+#define ASX_MT_C128_4K 1024  // the same for c128 P == 4096 (two CTAs per SM: config 1a 0.262 -> 0.242 ms)
 #endif
 template <int P, typename Real> struct Cfg {
   static constexpr bool DBL = sizeof(Real) == 8;
@@ -66,7 +66,7 @@ template <int P, typename Real> struct Cfg {
                                          : (P == 16384 ? ASX_R_16K_C64 : ASX_R_BIG_C64);
   static constexpr int NT = P / R;
   static constexpr int TPB = (NT == 1) ? 64 : (NT >= 256 ? 1 : 256 / NT);
-  static constexpr int MT = DBL ? (P <= 4096 ? ASX_MT_C128_SMALL : ASX_MT_C128) : ASX_MT_C64;
+  static constexpr int MT = DBL ? (P == 4096 ? ASX_MT_C128_4K : ASX_MT_C128) : ASX_MT_C64;
   static constexpr int MINB = (MT / (NT * TPB)) > 1 ? (MT / (NT * TPB)) : 1;
   // α-FFT residues transformed together per thread (ILP for the latency-bound FP64 case)
   static constexpr int KR = (DBL && P == 4096) ? ASX_KR_C128_4K : ((!DBL && P == 8192) ? ASX_KR_C64_8K : 1);
