@@ -44,7 +44,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the non-production methods")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work for the baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target busy seconds per host core for the CPU baseline sample")
     return ap.parse_args()
 
 
@@ -196,10 +197,11 @@ def cpu_reference(key: str, target_seconds: float):
 
     w = WORKLOADS[key]
     cores = len(os.sched_getaffinity(0))
-    # calibrate one signal, then size the sample to ~target_seconds of CPU work
-    dt, _ = _cpu_worker((key, 0, 1))
-    per = max(dt, 1e-5)
-    sample = int(max(cores, min(w.batch, target_seconds / per)))
+    # calibrate on a few signals, then size the sample to ~target_seconds of
+    # busy time on every core (cores * target_seconds CPU-seconds in total)
+    dt, k = _cpu_worker((key, 0, 4))
+    per = max(dt / k, 1e-5)
+    sample = int(max(cores, min(w.batch, cores * target_seconds / per)))
     sample = max(cores, (sample // cores) * cores)
     chunks = [(key, i * sample // cores, (i + 1) * sample // cores) for i in range(cores)]
     ctx = mp.get_context("fork")
@@ -211,8 +213,8 @@ def cpu_reference(key: str, target_seconds: float):
     value = sample * w.m / busy
     return {"value": value, "unit": "complex points/s", "cores": cores, "kind": "port",
             "sample": f"{sample} of {w.batch} signals of config {key} (per-signal oracle port of "
-                      f"ref transform_samples/naive_forward, {cores} processes, {busy:.2f} s busy, "
-                      f"{wall:.2f} s wall)"}
+                      f"ref transform_samples/naive_forward, {cores} processes, {busy:.2f} s busy per "
+                      f"process, {sum(r[0] for r in res):.1f} CPU-s in total, {wall:.2f} s wall)"}
 
 
 # ----------------------------------------------------------------- GPU arm

@@ -43,6 +43,9 @@ extern thread_local LastLaunch g_last_launch;
 #ifndef ASX_R_4K_C128
 #define ASX_R_4K_C128 8  // values per thread for c128 P == 4096
 #endif
+#ifndef ASX_R_512_C64
+#define ASX_R_512_C64 16  // values per thread for c64 P == 512: one warp per transform
+#endif
 #ifndef ASX_KR_C128_4K
 #define ASX_KR_C128_4K 1
 #endif
@@ -60,8 +63,9 @@ extern thread_local LastLaunch g_last_launch;
 #endif
 template <int P, typename Real> struct Cfg {
   static constexpr bool DBL = sizeof(Real) == 8;
-  static constexpr int R = (P <= 32)     ? P
-                           : (P <= 2048) ? 8
+  static constexpr int R = (P <= 32)                 ? P
+                           : (P == 512 && !DBL) ? ASX_R_512_C64
+                           : (P <= 2048)        ? 8
                            : DBL         ? (P == 4096 ? ASX_R_4K_C128 : 16)
                                          : (P == 16384 ? ASX_R_16K_C64 : ASX_R_BIG_C64);
   static constexpr int NT = P / R;

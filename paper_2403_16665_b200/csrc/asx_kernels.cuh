@@ -75,7 +75,8 @@ __host__ __device__ constexpr size_t align_up(size_t v, size_t a) { return (v + 
 // agree on it through this helper).
 template <typename Real, int P, int NT, int KIND>
 constexpr bool persist_dbuf() {
-  return KIND == 1 && size_t(P) * sizeof(typename CT<Real>::T) <= ASX_DBUF_MAX_BYTES;
+  // warp teams (NT <= 32) protect the exchange with one __syncwarp instead
+  return KIND == 1 && size_t(P) * sizeof(typename CT<Real>::T) <= ASX_DBUF_MAX_BYTES && !(NT > 1 && NT <= 32);
 }
 
 template <typename Real, int P, int NT, int TPB, bool TS = false, int KR = 1, bool DBUF = false>
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         }
       }
       if (staged) {
-        __syncthreads();  // the whole row has been consumed
+        E::team_sync();  // the whole row has been consumed (by this team)
         if (t == 0 && u + stride < batch) {
           fence_proxy_async();
           mbar_expect_tx(bar, (uint32_t)row_bytes);
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
           }
         }
         if (staged && c0 + KR >= p.r) {
-          __syncthreads();
+          E::team_sync();
           if (t == 0 && u + stride < batch) {
             fence_proxy_async();
             mbar_expect_tx(bar, (uint32_t)row_bytes);
