@@ -102,6 +102,23 @@ def pcie_duplex(dev, mib=256, reps=3):
     return best_h2d, best_d2h
 
 
+def launched_kernel(method: str) -> str:
+    """Name of the kernel the last execute launched (asx_last_launch variant bits)."""
+    import ctypes
+
+    from paper_2403_16665_b200 import _lib
+
+    v = [ctypes.c_int() for _ in range(4)]
+    _lib.lib().asx_last_launch(*[ctypes.byref(c) for c in v])
+    variant = v[3].value >> 1
+    if method == "chirp" and variant == 2:
+        return "k_chirp_local<float> (group-local exchanges, csrc/asx_chirp_local.cuh)"
+    if method == "direct":
+        return "k_direct"
+    kind = "afft" if method == "fft" else "chirp"
+    return f"k_fft_persist<{kind}{', TMEM tables' if variant == 1 else ''}>"
+
+
 def profiled_traffic(config_key: str, method: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
     path = os.path.join(REPO, "profiles", "traffic.json")
@@ -273,6 +290,7 @@ def run_gpu(args):
     value = total * w.m / (ms_per_step / 1e3)
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / avg launch duration
     avg_launch_s = (tot_ms / args.steps) / 1e3
+    kernel_name = launched_kernel(plan.method)  # before other methods / the host path launch
     peak, peak_kind = measured_peaks()
     fpk, fpk_src = fp_peak(w.dtype)
     achieved = bytes_step / avg_launch_s / 1e9
@@ -369,8 +387,7 @@ def run_gpu(args):
                 else "fallback 6650 GB/s (B200_PROFILING.md)",
                 "bytes_alg_per_launch": bytes_step,
                 "flops_alg_per_launch": flops, "achieved_alg_tflops": flops / avg_launch_s / 1e12,
-                "kernel": {"fft": "k_fft_persist<afft>", "chirp": "k_fft_persist<chirp>",
-                           "direct": "k_direct"}[plan.method],
+                "kernel": kernel_name,
                 # the FP-side roofline of the same launches (configs 1b-4 are FP-bound)
                 "compute": {"pipe": "fp32" if w.dtype == "complex64" else "fp64",
                             "achieved_tflops": flops / avg_launch_s / 1e12, "peak_tflops": fpk,
