@@ -44,7 +44,8 @@ struct ChirpLocal {
   static constexpr int REG = 4 * SUB;   // one 1024-point sub-problem
   static constexpr int XB = 16 * REG;   // exchange buffer (complex elements)
   static constexpr int T2N = 3 * 256;   // W_1024^{n' k2}, k2 = 1..3, n' < 256
-  static constexpr int T3N = 15 * 16;   // W_256^{n'' k3}, k3 = 1..15, n'' < 16 (exact; [0..2] = seeds W^{4a n''} w/o ASX_CL_P3TAB)
+  static constexpr int T3S = 18;        // T3 row stride: 16-byte aligned rows, conflict-free 128-bit reads
+  static constexpr int T3N = 16 * T3S;  // row n'' < 16: W_256^{n'' k3} at column k3 (exact; chain variant: seeds)
   static constexpr int CPT = 64;        // TMEM columns per thread: H 32 | chirp 16 | P1 twiddles 16
   // position of element n (< 1024) of a sub-problem inside its region
   __host__ __device__ static constexpr int pos(int n) { return n + (n >> 8) * (SUB - 256); }
@@ -128,8 +129,10 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
   uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(stbar + 2);
 
   for (int e = t; e < L::T2N; e += L::NT) T2[e] = exact_w<C>((e & 255) * (e / 256 + 1), 1024);
-  for (int e = t; e < L::T3N; e += L::NT)
-    T3[e] = exact_w<C>((ASX_CL_P3TAB ? (e / 16 + 1) : (e < 48 ? 4 * (e / 16 + 1) : 0)) * (e & 15), 256);
+  for (int e = t; e < L::T3N; e += L::NT) {
+    const int row = e / L::T3S, col = e % L::T3S;  // n'', k3
+    T3[e] = exact_w<C>(ASX_CL_P3TAB ? (col < 16 ? row * col : 0) : (col >= 1 && col <= 3 ? 4 * col * row : 0), 256);
+  }
   const C w1c = exact_w<C>(n16, 256);  // P3 / Q2 base twiddle W_256^{n''} (chain variant)
   if (t == 0) {
     mbar_init(stbar, 1);
@@ -200,17 +203,23 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
   };
   // P3 / Q2: u[k3] *= W_256^{n'' k3} from the exact shared table (or chains)
   auto tw_p3 = [&](C (&u3)[16]) {
+    const C* row = T3 + L::T3S * n16;
     if (ASX_CL_P3TAB) {
 #pragma unroll
-      for (int r = 1; r < 16; ++r) u3[r] = cmul(u3[r], T3[(r - 1) * 16 + n16]);
+      for (int q = 0; q < 8; ++q) {
+        C w0, w1;
+        ld_pair(row + 2 * q, w0, w1);
+        if (q > 0) u3[2 * q] = cmul(u3[2 * q], w0);
+        u3[2 * q + 1] = cmul(u3[2 * q + 1], w1);
+      }
     } else {
       C w[8];
       w[0] = w1c;
       w[1] = cmul(w1c, w1c);
       w[2] = cmul(w[1], w1c);
-      w[3] = T3[n16];
-      w[4] = T3[16 + n16];
-      w[5] = T3[32 + n16];
+      w[3] = row[1];
+      w[4] = row[2];
+      w[5] = row[3];
       tw16_apply(u3, w);
     }
   };
