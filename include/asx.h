@@ -138,7 +138,8 @@ int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype
 /* Launch shape of the last FFT-family kernel this thread launched: grid,
  * block, dynamic shared memory; *staged bit 0 = rows TMA-staged, bits 1.. =
  * kernel variant (0 plain, 1 chirp tables in tensor memory, 2 the P = 16384
- * complex64 group-local chirp kernel k_chirp_local). */
+ * complex64 group-local chirp kernel k_chirp_local, 3 the α-FFT with two
+ * teams per CTA splitting one signal's residues). */
 int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged);
 
 const char* asx_strerror(int status);

@@ -429,6 +429,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     p->env.use_tmem = (no_tm && no_tm[0] == '1') ? 0 : 1;
     const char* no_loc = std::getenv("ASX_NO_LOCAL");
     p->env.use_local = (no_loc && no_loc[0] == '1') ? 0 : 1;
+    const char* no_split = std::getenv("ASX_NO_SPLIT");
+    p->env.use_split = (no_split && no_split[0] == '1') ? 0 : 1;
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) p->env.sms = v;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)

@@ -31,6 +31,15 @@
 #ifndef ASX_CL_P3TAB
 #define ASX_CL_P3TAB 1  // P3/Q2 twiddles from the full exact [15][16] table (else exact seeds + chain)
 #endif
+#ifndef ASX_CL_EXACTDIAG
+#define ASX_CL_EXACTDIAG 0  // diagnostic only: every P1/Q4 twiddle by FP64 sincospi (slow)
+#endif
+#ifndef ASX_CL_P1F64
+#define ASX_CL_P1F64 0  // P1/Q4 twiddles exactly rounded: W^t..W^4t kept in FP64, products on the FP64 pipe
+#endif
+#ifndef ASX_CL_P1COMP
+#define ASX_CL_P1COMP 1  // P1/Q4 twiddle products W^{4a} W^b with FMA error terms (~correctly rounded)
+#endif
 #ifndef ASX_CL_P1EXACT
 #define ASX_CL_P1EXACT 1  // P1/Q4 twiddles w, w^2, w^3 exact from TMEM (else w^2, w^3 by products)
 #endif
@@ -73,9 +82,19 @@ __device__ __forceinline__ C exact_w(int e, int L) {  // W_L^e rounded once from
   return mk(Rl(cs), Rl(-sn));
 }
 
+// Complex product whose components carry the exact residual of one of their
+// two products (FMA error-free transformation): nearly correctly rounded.
+template <typename C>
+__device__ __forceinline__ C cmul_acc(C a, C b) {
+  using Real = decltype(a.x);
+  const Real p1 = a.x * b.x, e1 = fma(a.x, b.x, -p1);
+  const Real p2 = a.x * b.y, e2 = fma(a.x, b.y, -p2);
+  return mk(fma(-a.y, b.y, p1) + e1, fma(a.y, b.x, p2) + e2);
+}
+
 // u[r] *= w^r (r < 16) from exact w, w^2, w^3 and exact seeds w^{4a}
-// (w = {w1, w2, w3, s1, s2, s3, -, -}): every applied twiddle is at most one
-// product of exact values.
+// (w = {w1, w2, w3, s1, s2, s3, -, -}): every applied twiddle is one
+// (compensated with ASX_CL_P1COMP) product of exactly rounded values.
 template <typename C>
 __device__ __forceinline__ void tw16_apply(C (&u)[16], const C (&w)[8]) {
   u[1] = cmul(u[1], w[0]);
@@ -85,9 +104,15 @@ __device__ __forceinline__ void tw16_apply(C (&u)[16], const C (&w)[8]) {
   for (int a = 1; a < 4; ++a) {
     const C w4a = w[2 + a];
     u[4 * a] = cmul(u[4 * a], w4a);
-    u[4 * a + 1] = cmul(u[4 * a + 1], cmul(w4a, w[0]));
-    u[4 * a + 2] = cmul(u[4 * a + 2], cmul(w4a, w[1]));
-    u[4 * a + 3] = cmul(u[4 * a + 3], cmul(w4a, w[2]));
+    if (ASX_CL_P1COMP) {
+      u[4 * a + 1] = cmul(u[4 * a + 1], cmul_acc(w4a, w[0]));
+      u[4 * a + 2] = cmul(u[4 * a + 2], cmul_acc(w4a, w[1]));
+      u[4 * a + 3] = cmul(u[4 * a + 3], cmul_acc(w4a, w[2]));
+    } else {
+      u[4 * a + 1] = cmul(u[4 * a + 1], cmul(w4a, w[0]));
+      u[4 * a + 2] = cmul(u[4 * a + 2], cmul(w4a, w[1]));
+      u[4 * a + 3] = cmul(u[4 * a + 3], cmul(w4a, w[2]));
+    }
   }
 }
 
@@ -166,9 +191,22 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       tmem_st8(tbase + j0 * WPC, wh);
       if (j0 < 8) tmem_st8(tbase + 32 + j0 * WPC, wc);
     }
-    // P1 / Q4 twiddles of W = W_16384^t: {W, W^2, W^3, W^4, W^8, W^12} (exact)
+    // P1 / Q4 twiddles of W = W_16384^t: FP64 {W, W^2, W^3, W^4} (ASX_CL_P1F64),
+    // else FP32 {W, W^2, W^3, W^4, W^8, W^12} (exactly rounded)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 2 && ASX_CL_P1F64; ++h) {
+      uint32_t ws[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = (2 * h + k + 1) * t;
+        double sn, cs;
+        sincospi(2.0 * double(e & (L::P - 1)) / double(L::P), &sn, &cs);
+        c_to_words(make_double2(cs, -sn), &ws[4 * k]);
+      }
+      tmem_st8(tbase + 48 + 8 * h, ws);
+    }
+#pragma unroll
+    for (int h = 0; h < 2 && !ASX_CL_P1F64; ++h) {
       uint32_t ws[8];
 #pragma unroll
       for (int k = 0; k < CPC; ++k) {
@@ -192,6 +230,33 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     tmem_ld8(tbase + col, w);
 #pragma unroll
     for (int k = 0; k < CPC; ++k) out[k] = words_to_c(&w[k * WPC], (C*)nullptr);
+  };
+  // FP64 P1/Q4 twiddles: u[4a + b] *= round32(W^{4a} W^b), products in FP64
+  auto tw_p1_f64 = [&](C (&u)[16], const uint32_t (&wd)[16]) {
+    double2 w[4];  // W, W^2, W^3, W^4
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = words_to_c(&wd[4 * i], (double2*)nullptr);
+    auto f32 = [](double2 d) { return mk(Real(d.x), Real(d.y)); };
+#pragma unroll
+    for (int b = 1; b < 4; ++b) u[b] = cmul(u[b], f32(w[b - 1]));
+    double2 s4 = w[3];
+#pragma unroll
+    for (int a = 1; a < 4; ++a) {
+      u[4 * a] = cmul(u[4 * a], f32(s4));
+#pragma unroll
+      for (int b = 1; b < 4; ++b) u[4 * a + b] = cmul(u[4 * a + b], f32(cmul(s4, w[b - 1])));
+      if (a < 3) s4 = cmul(s4, w[3]);
+    }
+  };
+  auto ld_p1_f64 = [&](uint32_t (&wd)[16]) {
+    uint32_t a8[8], b8[8];
+    tmem_ld8(tbase + 48, a8);
+    tmem_ld8(tbase + 56, b8);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      wd[i] = a8[i];
+      wd[8 + i] = b8[i];
+    }
   };
   auto tw_p1 = [&](C (&w)[8]) {
     ld_tm(48, reinterpret_cast<C(&)[CPC]>(w[0]));
@@ -264,8 +329,19 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     dft_reg<16>(v);
     {
       C w[8];
-      tw_p1(w);
-      tw16_apply(v, w);
+      uint32_t wd[16];
+      if (ASX_CL_P1F64)
+        ld_p1_f64(wd);
+      else
+        tw_p1(w);
+      if (ASX_CL_P1F64) {
+        tw_p1_f64(v, wd);
+      } else if (ASX_CL_EXACTDIAG) {
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], exact_w<C>((r * t) & (L::P - 1), L::P));
+      } else {
+        tw16_apply(v, w);
+      }
     }
     // ---- G1: y_k1[t] -> region k1 (WAR: previous signal's Q4 reads)
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
@@ -358,14 +434,25 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) st_pair(rg + 2 * tau + 128 * h + L::SUB * i, v[4 * (2 * h) + i], v[4 * (2 * h + 1) + i]);
     C tw1[8];
-    tw_p1(tw1);
+    uint32_t twd[16];
+    if (ASX_CL_P1F64)
+      ld_p1_f64(twd);
+    else
+      tw_p1(tw1);
     __syncthreads();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
     __syncwarp();
     if ((t & 31) == 0) mbar_arrive(war);
     ++xcnt;
-    tw16_apply(v, tw1);
+    if (ASX_CL_P1F64) {
+      tw_p1_f64(v, twd);
+    } else if (ASX_CL_EXACTDIAG) {
+#pragma unroll
+      for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], exact_w<C>((r * t) & (L::P - 1), L::P));
+    } else {
+      tw16_apply(v, tw1);
+    }
     dft_reg<16>(v);
     {
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;

@@ -22,6 +22,7 @@ struct LaunchEnv {
   size_t smem_optin = 227 * 1024;
   int use_tmem = 1;  // chirp tables in tensor memory (env ASX_NO_TMEM=1 disables, for A/B runs)
   int use_local = 1; // P = 16384 complex64 chirp on k_chirp_local (env ASX_NO_LOCAL=1 disables)
+  int use_split = 1; // α-FFT residues split over two teams sharing a staged row (env ASX_NO_SPLIT=1 disables)
 };
 
 // Shape of the most recent launch on this thread (asx_last_launch, for
@@ -122,6 +123,31 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
     return c.per_sm;
   };
   if (G::NT == 1) kp.staged = 0;
+  if constexpr (KIND == KIND_AFFT && G::NT == 512 && size_t(P) * 2 * sizeof(Real) <= 65536) {
+    // two 512-thread teams per CTA split one signal's residues, one TMA-staged row
+    using LS = PersistLayout<Real, P, G::NT, 2, false, 1, DBUF, 1>;
+    auto ks = k_fft_persist<Real, P, G::NT, 2, KIND_AFFT, 1, false, 1, true>;
+    const size_t smem_s = LS::total(row_bytes, true, kp.tw_elems);
+    if (env.use_split && kp.r >= 2 && kp.staged && smem_s <= env.smem_optin) {
+      static thread_local int sp_attr_for = -1;
+      int dev_s = 0;
+      cudaGetDevice(&dev_s);
+      if (sp_attr_for != dev_s) {
+        cudaError_t e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
+        if (e != cudaSuccess) return e;
+        sp_attr_for = dev_s;
+      }
+      const int64_t grid_s = std::min<int64_t>(batch, env.sms);
+      kp.batch = batch;
+      ks<<<(unsigned)grid_s, 2 * G::NT, smem_s, st>>>(kp);
+      g_last_launch.tmem = 3;
+      g_last_launch.grid = (int)grid_s;
+      g_last_launch.block = 2 * G::NT;
+      g_last_launch.smem = (int)smem_s;
+      g_last_launch.staged = kp.staged;
+      return cudaGetLastError();
+    }
+  }
   if constexpr (KIND == KIND_CHIRP && sizeof(Real) == 4 && P == ChirpLocal::P) {
     // group-local exchange kernel (asx_chirp_local.cuh): one CTA per SM
     if (env.use_local && env.use_tmem && 2 * kp.m <= P && 2 * kp.n <= P && batch < (int64_t(1) << 31)) {

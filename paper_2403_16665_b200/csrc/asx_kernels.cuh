@@ -79,7 +79,7 @@ constexpr bool persist_dbuf() {
   return KIND == 1 && size_t(P) * sizeof(typename CT<Real>::T) <= ASX_DBUF_MAX_BYTES && !(NT > 1 && NT <= 32);
 }
 
-template <typename Real, int P, int NT, int TPB, bool TS = false, int KR = 1, bool DBUF = false>
+template <typename Real, int P, int NT, int TPB, bool TS = false, int KR = 1, bool DBUF = false, int NSTAGE = TPB>
 struct PersistLayout {
   using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS, DBUF>;
   using C = typename CT<Real>::T;
@@ -89,7 +89,7 @@ struct PersistLayout {
   }
   static constexpr size_t TAB_BYTES = align_up(size_t(E::TAB_ELEMS) * sizeof(C), 16);
   __host__ __device__ static size_t tab_off(size_t row_bytes, bool staged) {
-    return FFT_BYTES + size_t(TPB) * stage_bytes(row_bytes, staged);
+    return FFT_BYTES + size_t(NSTAGE) * stage_bytes(row_bytes, staged);
   }
   __host__ __device__ static size_t tw_off(size_t row_bytes, bool staged) {
     return tab_off(row_bytes, staged) + TAB_BYTES;
@@ -143,12 +143,17 @@ struct TmemCfg {
   static constexpr bool OK = (NTH % 128 == 0) && NEED <= 512;
 };
 
-template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1>
+// SPLIT (α-FFT only): the TPB teams of a CTA share ONE signal and split its
+// r output residues (team j takes c = j, j + TPB, ...); one TMA-staged row
+// serves them all, so a CTA of TPB teams keeps staging at full occupancy.
+template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1, bool SPLIT = false>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
+  static_assert(!SPLIT || (KIND == 0 && NT > 32), "SPLIT: alpha-FFT with CTA-wide team barriers");
   constexpr bool TS = TM && KIND == KIND_CHIRP;  // last-pass twiddle seeds in TMEM too
   constexpr bool DBUF = persist_dbuf<Real, P, NT, KIND>();
   using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS, DBUF>;
-  using L = PersistLayout<Real, P, NT, TPB, TS, KR, DBUF>;
+  using L = PersistLayout<Real, P, NT, TPB, TS, KR, DBUF, SPLIT ? 1 : TPB>;
+  constexpr int SIG_PER_CTA = SPLIT ? 1 : TPB;  // signals in flight per CTA
   using C = typename CT<Real>::T;
   constexpr int R = E::R;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -156,10 +161,12 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   const bool staged = p.staged != 0;
   const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(Real) : sizeof(C));
   C* fbuf = reinterpret_cast<C*>(smraw) + team * KR * E::SMEM_ELEMS;
-  unsigned char* stage = smraw + L::FFT_BYTES + team * L::stage_bytes(row_bytes, staged);
+  const int steam = SPLIT ? 0 : team;  // owner of the staged row / its mbarrier
+  unsigned char* stage = smraw + L::FFT_BYTES + steam * L::stage_bytes(row_bytes, staged);
   C* twa = reinterpret_cast<C*>(smraw + L::tw_off(row_bytes, staged));  // α pre-twiddle W_{rN} (afft, r > 1)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(
-                      smraw + align_up(L::tw_off(row_bytes, staged) + p.tw_elems * sizeof(C), 16)) + team;
+  uint64_t* const bar0 = reinterpret_cast<uint64_t*>(
+      smraw + align_up(L::tw_off(row_bytes, staged) + p.tw_elems * sizeof(C), 16));
+  uint64_t* bar = bar0 + steam;
 
   // per-thread pass twiddles -> registers; α pre-twiddle table -> shared
   typename E::TwRegs tr =
@@ -171,18 +178,19 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   }
   // batch < 2^31 (checked on the host): 32-bit signal indices keep the
   // persistent loop's live state small next to the 2R data registers
-  const int stride = int(gridDim.x) * TPB;
-  int u = int(blockIdx.x) * TPB + team;
+  const int stride = int(gridDim.x) * SIG_PER_CTA;
+  int u = int(blockIdx.x) * SIG_PER_CTA + (SPLIT ? 0 : team);
+  const bool stage_owner = t == 0 && (!SPLIT || team == 0);
   const int batch = int(p.batch);
   const int iters = (batch + stride - 1) / stride;
-  if (staged && t == 0) {
+  if (staged && stage_owner) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
   typename E::XSync xs;
-  E::xs_init(xs, bar - team + TPB, NT * TPB);
+  E::xs_init(xs, bar0 + TPB, NT * TPB);
   __syncthreads();
-  if (staged && t == 0 && u < batch) {
+  if (staged && stage_owner && u < batch) {
     mbar_expect_tx(bar, (uint32_t)row_bytes);
     tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * (row_bytes / p.n),
                 (uint32_t)row_bytes, bar);
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   const C* H = reinterpret_cast<const C*>(p.H);
   using TMC = TmemCfg<Real, NT * TPB, R, E::TSEED_COLS>;
   uint32_t tbase = 0;
-  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar - team + TPB + 1);  // after the mbarriers
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bar0 + TPB + 1);  // after the mbarriers
   if constexpr (TM) {
     static_assert(TMC::OK, "TMEM tables need a CTA of 128k threads within 512 columns");
     const int warp = threadIdx.x >> 5;
@@ -308,7 +316,9 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
       }
       // KR output residues at a time: their transforms share twiddles and
       // barriers and interleave in the pipeline (ILP)
-      for (int c0 = 0; c0 < p.r; c0 += KR) {
+      // uniform trip count over the CTA (the team barriers are CTA-wide)
+      for (int cb = 0; cb < p.r; cb += KR * (SPLIT ? TPB : 1)) {
+        const int c0 = cb + (SPLIT ? team * KR : 0);
         C v[KR][R];
 #pragma unroll
         for (int k = 0; k < KR; ++k) {
@@ -336,9 +346,12 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
             v[k][i] = val;
           }
         }
-        if (staged && c0 + KR >= p.r) {
-          E::team_sync();
-          if (t == 0 && u + stride < batch) {
+        if (staged && cb + KR * (SPLIT ? TPB : 1) >= p.r) {
+          if constexpr (SPLIT)
+            __syncthreads();  // every team has consumed the shared row
+          else
+            E::team_sync();
+          if (stage_owner && u + stride < batch) {
             fence_proxy_async();
             mbar_expect_tx(bar, (uint32_t)row_bytes);
             tma_load_1d(stage,
