@@ -123,8 +123,10 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
     return c.per_sm;
   };
   if (G::NT == 1) kp.staged = 0;
-  if constexpr (KIND == KIND_AFFT && G::NT == 512 && size_t(P) * 2 * sizeof(Real) <= 65536) {
+  if constexpr (KIND == KIND_AFFT && G::NT == 512 && sizeof(Real) == 4 && size_t(P) * 2 * sizeof(Real) <= 65536) {
     // two 512-thread teams per CTA split one signal's residues, one TMA-staged row
+    // (complex64 P = 8192: config 4 alpha-FFT 19.2 -> 17.5 ms; complex128 P = 4096
+    // measured slower than two independent CTAs per SM: 0.260 vs 0.242 ms)
     using LS = PersistLayout<Real, P, G::NT, 2, false, 1, DBUF, 1>;
     auto ks = k_fft_persist<Real, P, G::NT, 2, KIND_AFFT, 1, false, 1, true>;
     const size_t smem_s = LS::total(row_bytes, true, kp.tw_elems);
