@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
 #pragma unroll
     for (int r = 1; r < 16; ++r) w[r - 1] = T3[(r - 1) * 16 + n16];
   };
+  const bool fast_in = staged && !p.real_in && p.n >= L::P / 2;  // uniform over the CTA
+  const bool fast_out = p.m >= L::P / 2;
   C* const rg = xb + gk * L::REG;             // this group's region
   C* const sb = rg + k2 * L::SUB;             // this half-warp's sub-block
 
@@ -319,10 +321,15 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     for (int j0 = 0; j0 < 8; j0 += CPC) {
       C cw[CPC];
       ld_tm(32 + j0 * WPC, cw);
+      if (fast_in && live) {  // full complex row staged in shared memory: no per-element checks
 #pragma unroll
-      for (int k = 0; k < CPC; ++k) {
-        const int nn = t + 1024 * (j0 + k);
-        if (live && nn < p.n) v[j0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+        for (int k = 0; k < CPC; ++k) v[j0 + k] = cmul(reinterpret_cast<const C*>(stage)[t + 1024 * (j0 + k)], cw[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < CPC; ++k) {
+          const int nn = t + 1024 * (j0 + k);
+          if (live && nn < p.n) v[j0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+        }
       }
     }
     // ---- P1: radix-16 DIF over x[t + 1024 i] (upper half zero), twiddle W_16384^{t k1}
@@ -460,10 +467,15 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       for (int j0 = 0; j0 < 8; j0 += CPC) {
         C cw[CPC];
         ld_tm(32 + j0 * WPC, cw);
+        if (fast_out && live) {
 #pragma unroll
-        for (int k = 0; k < CPC; ++k) {
-          const int mm = t + 1024 * (j0 + k);
-          if (live && mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+          for (int k = 0; k < CPC; ++k) X[t + 1024 * (j0 + k)] = cmul(cconj(v[j0 + k]), cw[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < CPC; ++k) {
+            const int mm = t + 1024 * (j0 + k);
+            if (live && mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+          }
         }
       }
     }
