@@ -263,10 +263,16 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
       for (int j0 = 0; j0 < RIN; j0 += (TMC::CPC < RIN ? TMC::CPC : RIN)) {
         C cw[TMC::CPC];
         tab_chunk(1, j0, cw);
+        if (staged && !p.real_in && p.n >= NT * RIN && live) {  // full staged row: no per-element checks
 #pragma unroll
-        for (int k = 0; k < TMC::CPC && j0 + k < RIN; ++k) {
-          const int nn = t + NT * (j0 + k);
-          if (live && nn < p.n) v[j0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+          for (int k = 0; k < TMC::CPC && j0 + k < RIN; ++k)
+            v[j0 + k] = cmul(reinterpret_cast<const C*>(stage)[t + NT * (j0 + k)], cw[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < TMC::CPC && j0 + k < RIN; ++k) {
+            const int nn = t + NT * (j0 + k);
+            if (live && nn < p.n) v[j0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+          }
         }
       }
       if (staged) {
@@ -302,10 +308,15 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         for (int j0 = 0; j0 < ROUT; j0 += (TMC::CPC < ROUT ? TMC::CPC : ROUT)) {
           C cw[TMC::CPC];
           tab_chunk(1, j0, cw);
+          if (p.m >= NT * ROUT && live) {
 #pragma unroll
-          for (int k = 0; k < TMC::CPC && j0 + k < ROUT; ++k) {
-            const int mm = t + NT * (j0 + k);
-            if (live && mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+            for (int k = 0; k < TMC::CPC && j0 + k < ROUT; ++k) X[t + NT * (j0 + k)] = cmul(cconj(v[j0 + k]), cw[k]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < TMC::CPC && j0 + k < ROUT; ++k) {
+              const int mm = t + NT * (j0 + k);
+              if (live && mm < p.m) X[mm] = cmul(cconj(v[j0 + k]), cw[k]);
+            }
           }
         }
       }
