@@ -1,0 +1,218 @@
+// asx_afft_local.cuh — α-FFT for complex128 N = 4096 at α = 1/2 (reference
+// DenseFactor(2), BASELINE config 1a) with group-local exchanges.
+//
+// The α-FFT splits the bins m = c + 2d into two output residues c ∈ {0, 1};
+// residue c is the N-point DFT of x_n W_{2N}^{c n} (fastpath.py:162-181
+// even/odd recursion restated per residue).  One CTA of two
+// 256-thread teams transforms one signal at a time: team c computes residue
+// c, both teams read the same TMA-staged input row.  Each 4096-point DFT is
+// decimation in time over n = n0 + 16 n1 + 256 n2, d = g0 + 16 g1 + 256 g2:
+//
+//   S1  thread t = n0 + 16 n1 reads x[t + 256 n2] (the staged row, conflict-
+//       free), × W_32^{c n2} (compile-time constants), radix-16 over n2 -> g0,
+//       × W_{8192}^{t (c + 2 g0)} (exact, tensor memory)
+//   E1  team-wide exchange (named barrier): -> thread (n0, g0)
+//   S2  radix-16 over n1 -> g1, × W_256^{n0 g1} (exact, tensor memory)
+//   E2  exchange inside the half-warp (__syncwarp): -> thread (g1, g0)
+//   S3  radix-16 over n0 -> g2; only g2 < 8 (d < N/2, i.e. m < N) is stored
+//
+// Per residue: one team-wide and one half-warp exchange (the Stockham engine
+// needs three team-wide ones at R = 8), the α pre-twiddle folded into the
+// S1 constants and the S1 twiddle table, and every FP64 operation is
+// butterfly or twiddle work (no twiddle generation in the signal loop).
+#pragma once
+
+#include "asx_kernels.cuh"
+
+namespace asx {
+
+struct AfftLocal {
+  static constexpr int P = 4096, TNT = 256, NTH = 512;
+  static constexpr int RS = 272;        // region stride: 256 (E1) / 16 x 17 (E2) slots, conflict-free 16 B access
+  static constexpr int XB = 16 * RS;    // one team's exchange buffer (complex128 elements)
+  static constexpr size_t STAGE_OFF = size_t(2) * XB * sizeof(double2);
+  static constexpr size_t ROW_BYTES = size_t(P) * sizeof(double2);
+  static constexpr size_t BAR_OFF = STAGE_OFF + ROW_BYTES;
+  static constexpr size_t SMEM = BAR_OFF + 4 * sizeof(uint64_t) + 16;  // full, consumed, war[2], TMEM slot
+  static constexpr int CPT = 128;       // TMEM columns per thread: S1 twiddles 16 x 4 | S2 twiddles 16 x 4
+};
+
+__device__ __forceinline__ double2 tw_global_rt(const double2* __restrict__ g, int k, int lf) {
+  return cmul(__ldg(g + (k & ((1 << lf) - 1))), __ldg(g + (1 << lf) + (k >> lf)));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+// v[j] *= (twiddle j of this thread's 16-value TMEM block at column col), j >= J0
+template <int J0>
+__device__ __forceinline__ void afl_twiddle(double2 (&v)[16], uint32_t col) {
+#pragma unroll
+  for (int j0 = 0; j0 < 16; j0 += 4) {
+    if (j0 + 3 < J0) continue;
+    uint32_t w[16];
+    tmem_ld16(col + 4 * j0, w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (j0 + k >= J0) v[j0 + k] = cmul(v[j0 + k], words_to_c(&w[4 * k], (double2*)nullptr));
+  }
+}
+
+// One signal's residue CR on this team (t = team-local thread).
+template <int CR>
+__device__ __forceinline__ void afl_residue(const KParams& p, double2* xb, const unsigned char* stage,
+                                            uint64_t* full, uint64_t* consumed, uint64_t* war, uint32_t tbase,
+                                            int t, int u, int it, int stride, bool live, uint32_t& phase,
+                                            uint32_t& xcnt) {
+  using L = AfftLocal;
+  using C = double2;
+  const int n0 = t & 15, hi = t >> 4;
+  C v[16];
+  if (live) {
+    mbar_wait(full, phase);
+    phase ^= 1;
+    const C* row = reinterpret_cast<const C*>(stage);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = row[t + 256 * i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = mk(0.0, 0.0);
+  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(consumed);  // this warp is done with the staged row
+  // ---- S1: × W_32^{c n2}, radix-16 over n2, × W_8192^{t (c + 2 g0)}
+  if constexpr (CR == 1) {
+#pragma unroll
+    for (int i = 1; i < 16; ++i) v[i] = tw_const<32>(v[i], i);
+  }
+  dft_reg<16>(v);
+  afl_twiddle<CR == 0 ? 1 : 0>(v, tbase);
+  // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's S3 reads
+  if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+#pragma unroll
+  for (int g0 = 0; g0 < 16; ++g0) xb[t + L::RS * g0] = v[g0];
+  asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");
+  if (CR == 0 && t == 0 && u + stride < int(p.batch)) {
+    // next row: as soon as both teams have read this one (team 1 started with team 0)
+    mbar_wait(consumed, it & 1);
+    fence_proxy_async();
+    mbar_expect_tx(full, (uint32_t)L::ROW_BYTES);
+    tma_load_1d(const_cast<unsigned char*>(stage),
+                static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * int64_t(sizeof(C)),
+                (uint32_t)L::ROW_BYTES, full);
+  }
+  C* rg = xb + L::RS * hi;  // this half-warp's region (g0 = hi)
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) v[n1] = rg[n0 + 16 * n1];
+  __syncwarp();
+  // ---- S2: radix-16 over n1, × W_256^{n0 g1}
+  dft_reg<16>(v);
+  afl_twiddle<1>(v, tbase + 64);
+  // ---- E2 (half-warp): (n0, g1) -> thread (g1 = t & 15, g0)
+#pragma unroll
+  for (int g1 = 0; g1 < 16; ++g1) rg[n0 + 17 * g1] = v[g1];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = rg[j + 17 * n0];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(war);
+  ++xcnt;
+  // ---- S3: radix-16 over n0 -> g2; bins d = hi + 16 n0 + 256 g2 < 2048
+  dft_reg<16>(v);
+  if (live) {
+    C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+    const int dbase = hi + 16 * n0;
+    if (p.m >= L::P) {
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) X[CR + 2 * (dbase + 256 * g2)] = v[g2];
+    } else {
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) {
+        const int mm = CR + 2 * (dbase + 256 * g2);
+        if (mm < p.m) X[mm] = v[g2];
+      }
+    }
+  }
+}
+
+// Launch: grid <= #SMs, NTH threads, AfftLocal::SMEM dynamic shared memory.
+// Preconditions (host): complex128 input, n = 4096, r = 2, fold = 1,
+// m <= 4096, 16-byte aligned rows, batch < 2^31.
+template <typename Real>
+__global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
+  static_assert(sizeof(Real) == 8, "complex128 kernel");
+  using L = AfftLocal;
+  using C = double2;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int tid = threadIdx.x, team = tid >> 8, t = tid & 255, warp = tid >> 5;
+  C* xb = reinterpret_cast<C*>(smraw) + team * L::XB;
+  unsigned char* stage = smraw + L::STAGE_OFF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + L::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* consumed = bars + 1;
+  uint64_t* war = bars + 2 + team;
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 4);
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_init(consumed, L::NTH / 32);
+    mbar_init(bars + 2, L::TNT / 32);
+    mbar_init(bars + 3, L::TNT / 32);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * L::CPT);
+  {
+    // S1: W_8192^{t (c + 2 g0)}; S2: W_256^{n0 g1} = W_8192^{32 n0 g1}; from the plan's
+    // two-level W_{rN} table (one product of exactly rounded values)
+    const C* twa = reinterpret_cast<const C*>(p.twA);
+    const int c = team, n0 = t & 15;
+#pragma unroll
+    for (int j0 = 0; j0 < 16; j0 += 2) {
+      uint32_t w1[8], w2[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        c_to_words(tw_global_rt(twa, (t * (c + 2 * (j0 + k))) & (2 * L::P - 1), p.lfA), &w1[4 * k]);
+        c_to_words(tw_global_rt(twa, (32 * n0 * (j0 + k)) & (2 * L::P - 1), p.lfA), &w2[4 * k]);
+      }
+      tmem_st8(tbase + 4 * j0, w1);
+      tmem_st8(tbase + 64 + 4 * j0, w2);
+    }
+    tmem_wait_st();
+  }
+  __syncthreads();
+  const int stride = int(gridDim.x);
+  int u = int(blockIdx.x);
+  const int batch = int(p.batch);
+  const int iters = (batch + stride - 1) / stride;
+  if (tid == 0 && u < batch) {
+    mbar_expect_tx(full, (uint32_t)L::ROW_BYTES);
+    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * int64_t(sizeof(C)),
+                (uint32_t)L::ROW_BYTES, full);
+  }
+  uint32_t phase = 0, xcnt = 0;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it, u += stride) {
+    const bool live = u < batch;
+    if (team == 0)
+      afl_residue<0>(p, xb, stage, full, consumed, war, tbase, t, u, it, stride, live, phase, xcnt);
+    else
+      afl_residue<1>(p, xb, stage, full, consumed, war, tbase, t, u, it, stride, live, phase, xcnt);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(tmem_slot, 512);
+}
+
+}  // namespace asx

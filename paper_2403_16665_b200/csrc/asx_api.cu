@@ -431,6 +431,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     p->env.use_local = (no_loc && no_loc[0] == '1') ? 0 : 1;
     const char* no_split = std::getenv("ASX_NO_SPLIT");
     p->env.use_split = (no_split && no_split[0] == '1') ? 0 : 1;
+    const char* no_afl = std::getenv("ASX_NO_AFFT_LOCAL");
+    p->env.use_afl = (no_afl && no_afl[0] == '1') ? 0 : 1;
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) p->env.sms = v;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)

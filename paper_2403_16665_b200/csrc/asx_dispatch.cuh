@@ -10,6 +10,7 @@
 #include <cstdlib>
 
 #include "../../include/asx.h"
+#include "asx_afft_local.cuh"
 #include "asx_chirp2h.cuh"
 #include "asx_chirp_local.cuh"
 #include "asx_large.cuh"
@@ -23,6 +24,7 @@ struct LaunchEnv {
   int use_tmem = 1;  // chirp tables in tensor memory (env ASX_NO_TMEM=1 disables, for A/B runs)
   int use_local = 1; // P = 16384 complex64 chirp on k_chirp_local (env ASX_NO_LOCAL=1 disables)
   int use_split = 1; // α-FFT residues split over two teams sharing a staged row (env ASX_NO_SPLIT=1 disables)
+  int use_afl = 1;   // complex128 N = 4096, α = 1/2 α-FFT on k_afft_local (env ASX_NO_AFFT_LOCAL=1 disables)
 };
 
 // Shape of the most recent launch on this thread (asx_last_launch, for
@@ -147,6 +149,30 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
       g_last_launch.block = 2 * G::NT;
       g_last_launch.smem = (int)smem_s;
       g_last_launch.staged = kp.staged;
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (KIND == KIND_AFFT && sizeof(Real) == 8 && P == AfftLocal::P) {
+    // group-local α-FFT kernel (asx_afft_local.cuh): one CTA (two residue teams) per SM
+    if (env.use_afl && kp.r == 2 && kp.fold == 1 && !kp.real_in && kp.n == P && kp.m <= P && kp.staged &&
+        batch < (int64_t(1) << 31) && AfftLocal::SMEM <= env.smem_optin) {
+      auto ka = k_afft_local<double>;
+      static thread_local int afl_attr_for = -1;
+      int dev_a = 0;
+      cudaGetDevice(&dev_a);
+      if (afl_attr_for != dev_a) {
+        cudaError_t e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AfftLocal::SMEM);
+        if (e != cudaSuccess) return e;
+        afl_attr_for = dev_a;
+      }
+      const int64_t grid_a = std::min<int64_t>(batch, env.sms);
+      kp.batch = batch;
+      ka<<<(unsigned)grid_a, AfftLocal::NTH, AfftLocal::SMEM, st>>>(kp);
+      g_last_launch.tmem = 4;
+      g_last_launch.grid = (int)grid_a;
+      g_last_launch.block = AfftLocal::NTH;
+      g_last_launch.smem = (int)AfftLocal::SMEM;
+      g_last_launch.staged = 1;
       return cudaGetLastError();
     }
   }
