@@ -14,15 +14,30 @@
 //   E1  team-wide exchange (named barrier): -> thread (n0, g0)
 //   S2  radix-16 over n1 -> g1, × W_256^{n0 g1} (exact, tensor memory)
 //   E2  exchange inside the half-warp (__syncwarp): -> thread (g1, g0)
-//   S3  radix-16 over n0 -> g2; only g2 < 8 (d < N/2, i.e. m < N) is stored
+//   S3  radix-16 over n0 -> g2; only g2 < 8 (d < N/2, i.e. m < N) is kept
+//   OUT both teams park their bins in their own half-warp regions, one CTA
+//       barrier, then all 512 threads write X[e] with e contiguous across the
+//       warp (full 32-byte sectors: the residues interleave as m = c + 2d)
 //
 // Per residue: one team-wide and one half-warp exchange (the Stockham engine
 // needs three team-wide ones at R = 8), the α pre-twiddle folded into the
 // S1 constants and the S1 twiddle table, and every FP64 operation is
-// butterfly or twiddle work (no twiddle generation in the signal loop).
+// butterfly or twiddle work (no twiddle generation in the signal loop).  The
+// per-thread twiddles come from a plan-time image (k_afl_image), copied into
+// tensor memory once per CTA.
 #pragma once
 
 #include "asx_kernels.cuh"
+
+#ifndef ASX_AFL_OUT
+#define ASX_AFL_OUT 0  // 0: CTA-wide copy-out (full sectors); 1: per-team copy-out (teams decoupled)
+#endif
+#ifndef ASX_AFL_LAG
+#define ASX_AFL_LAG 0  // (ASX_AFL_OUT 1) team 1 starts a signal after team 0's S1 butterflies
+#endif
+#ifndef ASX_AFL_DBG
+#define ASX_AFL_DBG 0  // timing experiments only (wrong results): 1 no output, 2 no E1, 4 no E2, 8 no twiddle image
+#endif
 
 namespace asx {
 
@@ -33,12 +48,26 @@ struct AfftLocal {
   static constexpr size_t STAGE_OFF = size_t(2) * XB * sizeof(double2);
   static constexpr size_t ROW_BYTES = size_t(P) * sizeof(double2);
   static constexpr size_t BAR_OFF = STAGE_OFF + ROW_BYTES;
-  static constexpr size_t SMEM = BAR_OFF + 4 * sizeof(uint64_t) + 16;  // full, consumed, war[2], TMEM slot
+  static constexpr size_t SMEM = BAR_OFF + 5 * sizeof(uint64_t) + 16;  // full, consumed, war[2], lag, TMEM slot
   static constexpr int CPT = 128;       // TMEM columns per thread: S1 twiddles 16 x 4 | S2 twiddles 16 x 4
+  static constexpr int IMG_ELEMS = 32 * NTH;  // twiddle image: [j < 32][thread < 512] complex128
+  // parked output bin (g1, g2) of half-warp region hi of team c (conflict-free both ways)
+  __host__ __device__ static constexpr int out_pos(int c, int hi, int g1, int g2) {
+    return RS * hi + ((hi + 4 * c) & 7) + g1 + 16 * g2;
+  }
 };
 
-__device__ __forceinline__ double2 tw_global_rt(const double2* __restrict__ g, int k, int lf) {
-  return cmul(__ldg(g + (k & ((1 << lf) - 1))), __ldg(g + (1 << lf) + (k >> lf)));
+// Plan-time image of every thread's tensor-memory twiddles (exact FP64
+// sincospi of W_8192^k): img[j][tid], j < 16: W_8192^{t (c + 2 j)} (S1 of
+// team c = tid / 256, t = tid % 256); j >= 16: W_256^{n0 (j - 16)}, n0 = t % 16.
+static __global__ void k_afl_image(double2* img) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= AfftLocal::IMG_ELEMS) return;
+  const int j = i / AfftLocal::NTH, tid = i % AfftLocal::NTH, c = tid / 256, t = tid % 256;
+  const int k = j < 16 ? (t * (c + 2 * j)) & 8191 : (32 * (t & 15) * (j - 16)) & 8191;
+  double sn, cs;
+  sincospi(2.0 * double(k) / 8192.0, &sn, &cs);
+  img[i] = make_double2(cs, -sn);
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -66,20 +95,28 @@ __device__ __forceinline__ void afl_twiddle(double2 (&v)[16], uint32_t col) {
   }
 }
 
-// One signal's residue CR on this team (t = team-local thread).
+struct AflCtx {
+  double2* xb;  // this team's exchange buffer
+  const unsigned char* stage;
+  uint64_t *full, *consumed, *war, *lag;
+  uint32_t tbase;
+  int t;
+};
+
+// One signal's residue CR on this team (t = team-local thread), up to the
+// parked outputs.
 template <int CR>
-__device__ __forceinline__ void afl_residue(const KParams& p, double2* xb, const unsigned char* stage,
-                                            uint64_t* full, uint64_t* consumed, uint64_t* war, uint32_t tbase,
-                                            int t, int u, int it, int stride, bool live, uint32_t& phase,
-                                            uint32_t& xcnt) {
+__device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, int u, int it, int stride,
+                                            bool live, uint32_t& phase, uint32_t xcnt) {
   using L = AfftLocal;
   using C = double2;
-  const int n0 = t & 15, hi = t >> 4;
+  const int t = cx.t, n0 = t & 15, hi = t >> 4;
   C v[16];
+  if (ASX_AFL_OUT == 1 && ASX_AFL_LAG && CR == 1) mbar_wait(cx.lag, it & 1);
   if (live) {
-    mbar_wait(full, phase);
+    mbar_wait(cx.full, phase);
     phase ^= 1;
-    const C* row = reinterpret_cast<const C*>(stage);
+    const C* row = reinterpret_cast<const C*>(cx.stage);
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = row[t + 256 * i];
   } else {
@@ -87,127 +124,164 @@ __device__ __forceinline__ void afl_residue(const KParams& p, double2* xb, const
     for (int i = 0; i < 16; ++i) v[i] = mk(0.0, 0.0);
   }
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(consumed);  // this warp is done with the staged row
+  if ((threadIdx.x & 31) == 0) mbar_arrive(cx.consumed);  // this warp is done with the staged row
   // ---- S1: × W_32^{c n2}, radix-16 over n2, × W_8192^{t (c + 2 g0)}
   if constexpr (CR == 1) {
 #pragma unroll
     for (int i = 1; i < 16; ++i) v[i] = tw_const<32>(v[i], i);
   }
   dft_reg<16>(v);
-  afl_twiddle<CR == 0 ? 1 : 0>(v, tbase);
-  // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's S3 reads
-  if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+  afl_twiddle<CR == 0 ? 1 : 0>(v, cx.tbase);
+  if (ASX_AFL_OUT == 1 && ASX_AFL_LAG && CR == 0) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.lag);
+  }
+  // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's output reads
+  if (xcnt) mbar_wait(cx.war, (xcnt - 1) & 1);
+  C* const xb = cx.xb;
+  if (!(ASX_AFL_DBG & 2)) {
 #pragma unroll
-  for (int g0 = 0; g0 < 16; ++g0) xb[t + L::RS * g0] = v[g0];
-  asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");
+    for (int g0 = 0; g0 < 16; ++g0) xb[t + L::RS * g0] = v[g0];
+    asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");
+  }
   if (CR == 0 && t == 0 && u + stride < int(p.batch)) {
-    // next row: as soon as both teams have read this one (team 1 started with team 0)
-    mbar_wait(consumed, it & 1);
+    // next row: both teams started this signal together and have read it by now
+    mbar_wait(cx.consumed, it & 1);
     fence_proxy_async();
-    mbar_expect_tx(full, (uint32_t)L::ROW_BYTES);
-    tma_load_1d(const_cast<unsigned char*>(stage),
+    mbar_expect_tx(cx.full, (uint32_t)L::ROW_BYTES);
+    tma_load_1d(const_cast<unsigned char*>(cx.stage),
                 static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * int64_t(sizeof(C)),
-                (uint32_t)L::ROW_BYTES, full);
+                (uint32_t)L::ROW_BYTES, cx.full);
   }
   C* rg = xb + L::RS * hi;  // this half-warp's region (g0 = hi)
+  if (!(ASX_AFL_DBG & 2)) {
 #pragma unroll
-  for (int n1 = 0; n1 < 16; ++n1) v[n1] = rg[n0 + 16 * n1];
-  __syncwarp();
+    for (int n1 = 0; n1 < 16; ++n1) v[n1] = rg[n0 + 16 * n1];
+    __syncwarp();
+  }
   // ---- S2: radix-16 over n1, × W_256^{n0 g1}
   dft_reg<16>(v);
-  afl_twiddle<1>(v, tbase + 64);
+  afl_twiddle<1>(v, cx.tbase + 64);
   // ---- E2 (half-warp): (n0, g1) -> thread (g1 = t & 15, g0)
+  if (!(ASX_AFL_DBG & 4)) {
 #pragma unroll
-  for (int g1 = 0; g1 < 16; ++g1) rg[n0 + 17 * g1] = v[g1];
-  __syncwarp();
+    for (int g1 = 0; g1 < 16; ++g1) rg[n0 + 17 * g1] = v[g1];
+    __syncwarp();
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = rg[j + 17 * n0];
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(war);
-  ++xcnt;
-  // ---- S3: radix-16 over n0 -> g2; bins d = hi + 16 n0 + 256 g2 < 2048
+    for (int j = 0; j < 16; ++j) v[j] = rg[j + 17 * n0];
+    __syncwarp();
+  }
+  // ---- S3: radix-16 over n0 -> g2; park bins d = hi + 16 n0 + 256 g2 < 2048
   dft_reg<16>(v);
-  if (live) {
-    C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
-    const int dbase = hi + 16 * n0;
-    if (p.m >= L::P) {
+  if (!(ASX_AFL_DBG & 1)) {
 #pragma unroll
-      for (int g2 = 0; g2 < 8; ++g2) X[CR + 2 * (dbase + 256 * g2)] = v[g2];
-    } else {
+    for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(ASX_AFL_OUT ? 0 : CR, hi, n0, g2)] = v[g2];
+  } else if (v[0].x == 12345.678) {
+    xb[0] = v[1];
+  }
+  if constexpr (ASX_AFL_OUT == 1) {
+    asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");  // this team's bins parked
+    if (live && !(ASX_AFL_DBG & 1)) {
+      C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
 #pragma unroll
-      for (int g2 = 0; g2 < 8; ++g2) {
-        const int mm = CR + 2 * (dbase + 256 * g2);
-        if (mm < p.m) X[mm] = v[g2];
+      for (int j = 0; j < 8; ++j) {
+        const int d = t + 256 * j, mm = CR + 2 * d;
+        const C val = xb[L::out_pos(0, d & 15, (d >> 4) & 15, d >> 8)];
+        if (p.m >= L::P || mm < p.m) X[mm] = val;
       }
     }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
   }
 }
 
 // Launch: grid <= #SMs, NTH threads, AfftLocal::SMEM dynamic shared memory.
 // Preconditions (host): complex128 input, n = 4096, r = 2, fold = 1,
-// m <= 4096, 16-byte aligned rows, batch < 2^31.
+// m <= 4096, 16-byte aligned rows, batch < 2^31, p.afl = the plan's image.
 template <typename Real>
 __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
   static_assert(sizeof(Real) == 8, "complex128 kernel");
   using L = AfftLocal;
   using C = double2;
   extern __shared__ __align__(128) unsigned char smraw[];
-  const int tid = threadIdx.x, team = tid >> 8, t = tid & 255, warp = tid >> 5;
-  C* xb = reinterpret_cast<C*>(smraw) + team * L::XB;
-  unsigned char* stage = smraw + L::STAGE_OFF;
+  const int tid = threadIdx.x, team = tid >> 8, warp = tid >> 5;
+  C* const xb0 = reinterpret_cast<C*>(smraw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + L::BAR_OFF);
-  uint64_t* full = bars;
-  uint64_t* consumed = bars + 1;
-  uint64_t* war = bars + 2 + team;
-  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 4);
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(bars + 5);
+  AflCtx cx;
+  cx.xb = xb0 + team * L::XB;
+  cx.stage = smraw + L::STAGE_OFF;
+  cx.full = bars;
+  cx.consumed = bars + 1;
+  cx.war = bars + 2 + (ASX_AFL_OUT ? team : 0);
+  cx.lag = bars + 4;
+  cx.t = tid & 255;
+  const int stride = int(gridDim.x);
+  int u = int(blockIdx.x);
+  const int batch = int(p.batch);
+  const int iters = (batch + stride - 1) / stride;
   if (tid == 0) {
-    mbar_init(full, 1);
-    mbar_init(consumed, L::NTH / 32);
-    mbar_init(bars + 2, L::TNT / 32);
+    mbar_init(cx.full, 1);
+    mbar_init(cx.consumed, L::NTH / 32);
+    mbar_init(bars + 2, (ASX_AFL_OUT ? L::TNT : L::NTH) / 32);
     mbar_init(bars + 3, L::TNT / 32);
+    mbar_init(bars + 4, L::TNT / 32);
     fence_mbar_init();
+    if (u < batch) {  // first row in flight while the twiddles go to tensor memory
+      mbar_expect_tx(cx.full, (uint32_t)L::ROW_BYTES);
+      tma_load_1d(const_cast<unsigned char*>(cx.stage),
+                  static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * int64_t(sizeof(C)),
+                  (uint32_t)L::ROW_BYTES, cx.full);
+    }
   }
   if (warp == 0) tmem_alloc(&tmem_slot, 512);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * L::CPT);
+  cx.tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * L::CPT);
   {
-    // S1: W_8192^{t (c + 2 g0)}; S2: W_256^{n0 g1} = W_8192^{32 n0 g1}; from the plan's
-    // two-level W_{rN} table (one product of exactly rounded values)
-    const C* twa = reinterpret_cast<const C*>(p.twA);
-    const int c = team, n0 = t & 15;
+    const double2* img = reinterpret_cast<const double2*>(p.afl) + tid;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += 16) {
+      double2 w[16];
 #pragma unroll
-    for (int j0 = 0; j0 < 16; j0 += 2) {
-      uint32_t w1[8], w2[8];
+      for (int j = 0; j < 16; ++j) w[j] = (ASX_AFL_DBG & 8) ? mk(1.0, 0.0) : __ldg(img + L::NTH * (j0 + j));
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        c_to_words(tw_global_rt(twa, (t * (c + 2 * (j0 + k))) & (2 * L::P - 1), p.lfA), &w1[4 * k]);
-        c_to_words(tw_global_rt(twa, (32 * n0 * (j0 + k)) & (2 * L::P - 1), p.lfA), &w2[4 * k]);
+      for (int j = 0; j < 16; j += 2) {
+        uint32_t w8[8];
+        c_to_words(w[j], &w8[0]);
+        c_to_words(w[j + 1], &w8[4]);
+        tmem_st8(cx.tbase + 4 * (j0 + j), w8);
       }
-      tmem_st8(tbase + 4 * j0, w1);
-      tmem_st8(tbase + 64 + 4 * j0, w2);
     }
     tmem_wait_st();
   }
   __syncthreads();
-  const int stride = int(gridDim.x);
-  int u = int(blockIdx.x);
-  const int batch = int(p.batch);
-  const int iters = (batch + stride - 1) / stride;
-  if (tid == 0 && u < batch) {
-    mbar_expect_tx(full, (uint32_t)L::ROW_BYTES);
-    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * int64_t(sizeof(C)),
-                (uint32_t)L::ROW_BYTES, full);
-  }
   uint32_t phase = 0, xcnt = 0;
 #pragma unroll 1
   for (int it = 0; it < iters; ++it, u += stride) {
     const bool live = u < batch;
     if (team == 0)
-      afl_residue<0>(p, xb, stage, full, consumed, war, tbase, t, u, it, stride, live, phase, xcnt);
+      afl_residue<0>(p, cx, u, it, stride, live, phase, xcnt);
     else
-      afl_residue<1>(p, xb, stage, full, consumed, war, tbase, t, u, it, stride, live, phase, xcnt);
+      afl_residue<1>(p, cx, u, it, stride, live, phase, xcnt);
+    if (ASX_AFL_OUT == 0) __syncthreads();  // both residues parked
+    if (ASX_AFL_OUT == 0 && live && !(ASX_AFL_DBG & 1)) {
+      // X[e], e = c + 2d: contiguous across the warp, residue c = e & 1
+      C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+      const bool full_row = p.m >= L::P;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = tid + L::NTH * j, c = e & 1, d = e >> 1;
+        const C val = xb0[c * L::XB + L::out_pos(c, d & 15, (d >> 4) & 15, d >> 8)];
+        if (full_row || e < p.m) X[e] = val;
+      }
+    }
+    if (ASX_AFL_OUT == 0) {
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(cx.war);
+    }
+    ++xcnt;
   }
   tmem_fence_before();
   __syncthreads();

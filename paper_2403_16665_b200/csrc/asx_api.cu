@@ -84,6 +84,7 @@ struct asx_plan_s {
   void* tables = nullptr;
   size_t table_bytes = 0;
   size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
+  size_t off_afl = 0;  // k_afft_local twiddle image (complex128 N = 4096, alpha = 1/2), 0 = none
   int lfA = 0;
   int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
   // large chirp path (P > one CTA): four-step P = P1 x P2 through workspace A
@@ -188,6 +189,7 @@ void fill_kparams(const asx_plan_s* p, KParams& kp) {
   kp.W = base + p->off_W;
   kp.tw_elems = p->tw_elems;
   kp.chirp_len = std::max(p->n, p->m);
+  kp.afl = p->off_afl ? base + p->off_afl : nullptr;
 }
 
 void* large_workspace(asx_plan_s* p, cudaStream_t st) {
@@ -499,6 +501,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     A_sz = chirp_P;  // four-step workspace
   }
   if (chosen == ASX_DIRECT) W_sz = m * n;
+  const bool afl = chosen == ASX_FFT && dtype == ASX_C128 && p->P == AfftLocal::P && p->r == 2 && p->fold == 1;
+  const int64_t afl_sz = afl ? AfftLocal::IMG_ELEMS : 0;
   p->tw_elems = (int)twA_sz;  // shared-memory table: α pre-twiddle only
   auto align = [](size_t v) { return (v + 31) & ~size_t(31); };
   p->off_twP = 0;
@@ -525,6 +529,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   elems += align(cwc_sz);
   p->off_scratch = elems * es;
   elems += align(scratch_sz);
+  p->off_afl = afl_sz ? elems * es : 0;
+  elems += align(afl_sz);
   p->table_bytes = std::max<size_t>(elems * es, 64);
 
   cudaError_t e = cudaMalloc(&p->tables, p->table_bytes);
@@ -551,6 +557,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
         base + p->off_cw, base + p->off_cwc, n, m, (uint64_t)a, L2, (uint64_t)chirp_P, dbl);
   }
   if (twA_sz) fill_two_level(base + p->off_twA, p->r * p->P, p->lfA, dbl, st);
+  if (afl_sz) k_afl_image<<<(unsigned)((afl_sz + 255) / 256), 256, 0, st>>>(reinterpret_cast<double2*>(base + p->off_afl));
   double2* wP_d = nullptr;
   if (chosen == ASX_CHIRP) {
     const uint64_t L2 = 2ull * (uint64_t)d * (uint64_t)n;

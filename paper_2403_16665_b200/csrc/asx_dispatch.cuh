@@ -155,7 +155,7 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
   if constexpr (KIND == KIND_AFFT && sizeof(Real) == 8 && P == AfftLocal::P) {
     // group-local α-FFT kernel (asx_afft_local.cuh): one CTA (two residue teams) per SM
     if (env.use_afl && kp.r == 2 && kp.fold == 1 && !kp.real_in && kp.n == P && kp.m <= P && kp.staged &&
-        batch < (int64_t(1) << 31) && AfftLocal::SMEM <= env.smem_optin) {
+        kp.afl && batch < (int64_t(1) << 31) && AfftLocal::SMEM <= env.smem_optin) {
       auto ka = k_afft_local<double>;
       static thread_local int afl_attr_for = -1;
       int dev_a = 0;

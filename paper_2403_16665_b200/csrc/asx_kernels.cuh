@@ -44,6 +44,7 @@ struct KParams {
   int staged;          // 1: rows fetched by TMA into shared memory
   int tw_elems;        // shared twiddle elements (W_P two-level [+ W_rN two-level])
   int64_t chirp_len;   // entries of the chirp table (max(N, M))
+  const void* afl;     // k_afft_local: per-thread twiddle image for tensor memory (plan time), else null
 };
 
 template <typename C>
