@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the non-production methods")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the untimed-in-headline side measurement of config 1a (alpha-FFT recursion)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target busy seconds per host core for the CPU baseline sample")
     return ap.parse_args()
@@ -113,6 +115,8 @@ def launched_kernel(method: str) -> str:
     variant = v[3].value >> 1
     if method == "chirp" and variant == 2:
         return "k_chirp_local<float> (group-local exchanges, csrc/asx_chirp_local.cuh)"
+    if method == "fft" and variant == 4:
+        return "k_afft_local<double> (group-local alpha-FFT, csrc/asx_afft_local.cuh)"
     if method == "direct":
         return "k_direct"
     kind = "afft" if method == "fft" else "chirp"
@@ -236,6 +240,38 @@ def cpu_reference(key: str, target_seconds: float):
 
 # ----------------------------------------------------------------- GPU arm
 
+def side_config(key, dev, stream, peak, reps=20):
+    """Device time of another BASELINE config (method auto) with CUDA events on
+    the launch stream, after warm-up; inputs exceed L2."""
+    import torch
+
+    import paper_2403_16665_b200 as asx
+    from paper_2403_16665_b200.signals import WORKLOADS, generate_device
+
+    w = WORKLOADS[key]
+    x = generate_device(w, 0, w.batch, device=dev)
+    p = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, real_input=w.real, device=dev.index)
+    out = torch.empty((w.batch, w.m), dtype=getattr(torch, w.dtype), device=dev)
+    for _ in range(3):
+        p.execute(x, out=out)
+    torch.cuda.synchronize()
+    s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s_.record(stream)
+    for _ in range(reps):
+        p.execute(x, out=out)
+    e_.record(stream)
+    torch.cuda.synchronize()
+    ms = s_.elapsed_time(e_) / reps
+    kern = launched_kernel(p.method)
+    gbs = w.bytes_alg(w.batch) / (ms / 1e3) / 1e9
+    res = {"workload": f"config {w.key}: batch {w.batch} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
+           "method": p.method, "kernel": kern, "ms_per_step": ms, "value": w.batch * w.m / (ms / 1e3),
+           "unit": "complex points/s", "hbm_gbs": gbs, "hbm_frac": gbs / peak, "reps": reps}
+    del x, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_gpu(args):
     import numpy as np
     import torch
@@ -351,6 +387,13 @@ def run_gpu(args):
                            "how": "concurrent pinned 256 MiB copies on two streams, best of 3",
                            "bound_ms": bound_s * 1e3, "frac": bound_s / e2e_s}
 
+    # side measurement (world 1 only, not part of `value`): the batched α-FFT
+    # recursion itself on config 1a, the one BASELINE config whose op count
+    # lets the α-FFT approach the HBM roofline
+    other = {}
+    if world == 1 and not args.no_other_configs and args.config != "1a":
+        other["1a"] = side_config("1a", dev, stream, peak)
+
     # untimed verification collective: per-rank checksums gathered over NCCL
     checks = gather_checksums(out, device=dev)
 
@@ -397,6 +440,7 @@ def run_gpu(args):
                             else "reference alpha-FFT op count 6*mults+2*adds per signal (fastpath.py:113-127)"},
             },
             "other_methods": alt,
+            "other_configs": other,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * int(plan.info.kernels_per_execute),
