@@ -28,6 +28,9 @@
 
 #include "asx_kernels.cuh"
 
+#ifndef ASX_CL_DBG
+#define ASX_CL_DBG 0  // timing experiments only (wrong results): 1 no G1 barrier, 2 no Q4 barrier
+#endif
 #ifndef ASX_CL_P3TAB
 #define ASX_CL_P3TAB 1  // P3/Q2 twiddles from the full exact [15][16] table (else exact seeds + chain)
 #endif
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     for (int k1 = 0; k1 < 16; ++k1) xb[k1 * L::REG + L::pos(t)] = v[k1];
     C tw2[12];
     ld_t2(tw2);
-    __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
+    if (!(ASX_CL_DBG & 1)) __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
     if (staged && t == 0 && u + stride < batch) {
       fence_proxy_async();
       mbar_expect_tx(stbar, (uint32_t)row_bytes);
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       ld_p1_f64(twd);
     else
       tw_p1(tw1);
-    __syncthreads();
+    if (!(ASX_CL_DBG & 2)) __syncthreads();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
     __syncwarp();
