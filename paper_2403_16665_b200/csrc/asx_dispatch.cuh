@@ -334,7 +334,11 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kern) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) kern<<<(unsigned)P1, G::NT, smem, st>>>(lp);
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      cudaGetLastError();
+    if (e == cudaSuccess) kern<<<(unsigned)std::min<int64_t>(P1, sms), G::NT, smem, st>>>(lp);
   };
   if (mode == ROW_SPECTRUM)
     go(k_large_rows<Real, P2, G::NT, ROW_SPECTRUM>);

@@ -20,7 +20,18 @@
 
 namespace asx {
 
-constexpr int kColTile = 8;  // columns per CTA in the column kernels (8 x 16 B = 128 B rows)
+#ifndef ASX_COL_TILE
+#define ASX_COL_TILE 4
+#endif
+// columns per CTA in the column kernels: 4 x 16 B = 64 B row segments (two
+// full sectors); small enough for two CTAs per SM, so one CTA's gather
+// latency overlaps the other's butterflies (8 columns: 128 B rows but one
+// CTA per SM, config 2 0.163 ms per column pass)
+constexpr int kColTile = ASX_COL_TILE;
+template <int NT>
+constexpr int col_minb() {
+  return (1024 / (NT * kColTile)) < 1 ? 1 : (1024 / (NT * kColTile)) > 16 ? 16 : (1024 / (NT * kColTile));
+}
 
 struct LParams {
   const void* x;  // input row (real or complex), N samples
@@ -62,7 +73,7 @@ struct ColCfg {
 // 8 teams of NT threads, one column each; the tile passes through the teams'
 // shared buffers on the way in and out so HBM sees 128 B row segments.
 template <typename Real, int P1, int NT, int MODE>
-__global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
+__global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LParams p) {
   using E = Fft<Real, P1, NT>;
   using C = typename CT<Real>::T;
   constexpr int R = E::R;
@@ -137,51 +148,67 @@ __global__ void __launch_bounds__(NT* kColTile, 1) k_large_cols(LParams p) {
 
 enum { ROW_SPECTRUM = 0, ROW_MAIN = 1 };
 
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Persistent over rows (grid <= #SMs): while row k1 is transformed, the next
+// row of A (and of Ht) is prefetched into L2, so the row loads of one CTA per
+// SM wait on L2 instead of HBM.
 template <typename Real, int P2, int NT, int MODE>
 __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
   using E = Fft<Real, P2, NT>;
   using C = typename CT<Real>::T;
   constexpr int R = E::R;
+  constexpr uint32_t ROW_BYTES = uint32_t(P2) * sizeof(C);
   const uint64_t Pmask = uint64_t(p.P - 1);
   extern __shared__ __align__(128) unsigned char smraw[];
   C* sm = reinterpret_cast<C*>(smraw);
   const int t = threadIdx.x;
-  const int k1 = blockIdx.x;
+  const int rows = int(p.P / P2);
   const typename E::TwRegs tr =
       E::make_tw(t, reinterpret_cast<const C*>(p.twP2), sm + E::SMEM_ELEMS, threadIdx.x, NT);
   typename E::XSync xs;
   E::xs_init(xs, reinterpret_cast<uint64_t*>(sm + E::SMEM_ELEMS + E::TAB_ELEMS + (E::TAB_ELEMS & 1)), NT);
   __syncthreads();
-  C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * P2;
-  C v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = row[t + NT * i];
-  if constexpr (MODE == ROW_SPECTRUM) {
-    E::run(v, sm, t, tr, xs);
-    C* out = reinterpret_cast<C*>(p.Hout) + int64_t(k1) * P2;
-    const Real s = Real(p.scale);
-#pragma unroll
-    for (int i = 0; i < R; ++i) out[t + NT * i] = mk(v[i].x * s, v[i].y * s);
-  } else {
-    const C* ht = reinterpret_cast<const C*>(p.Ht) + int64_t(k1) * P2;
-    // one FFT body, two trips (forward step 3, then inverse step 1)
 #pragma unroll 1
-    for (int half = 0; half < 2; ++half) {
-      E::run(v, sm, t, tr, xs);
-      if (half == 0) {
+  for (int k1 = blockIdx.x; k1 < rows; k1 += gridDim.x) {
+    if (t == 0 && k1 + int(gridDim.x) < rows) {
+      const int64_t nxt = int64_t(k1 + gridDim.x) * P2;
+      prefetch_l2_bulk(reinterpret_cast<const C*>(p.A) + nxt, ROW_BYTES);
+      if (MODE == ROW_MAIN) prefetch_l2_bulk(reinterpret_cast<const C*>(p.Ht) + nxt, ROW_BYTES);
+    }
+    C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * P2;
+    C v[R];
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          v[i] = cconj(cmul(v[i], __ldg(ht + t + NT * i)));
-          if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+    for (int i = 0; i < R; ++i) v[i] = row[t + NT * i];
+    if constexpr (MODE == ROW_SPECTRUM) {
+      E::run(v, sm, t, tr, xs);
+      C* out = reinterpret_cast<C*>(p.Hout) + int64_t(k1) * P2;
+      const Real s = Real(p.scale);
+#pragma unroll
+      for (int i = 0; i < R; ++i) out[t + NT * i] = mk(v[i].x * s, v[i].y * s);
+    } else {
+      const C* ht = reinterpret_cast<const C*>(p.Ht) + int64_t(k1) * P2;
+      // one FFT body, two trips (forward step 3, then inverse step 1)
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        E::run(v, sm, t, tr, xs);
+        if (half == 0) {
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            v[i] = cconj(cmul(v[i], __ldg(ht + t + NT * i)));
+            if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+          }
         }
       }
-    }
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint64_t c = uint64_t(t + NT * i);
-      row[t + NT * i] =
-          cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(k1) * c) & Pmask, p.lfBig));
-      if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+      for (int i = 0; i < R; ++i) {
+        const uint64_t c = uint64_t(t + NT * i);
+        row[t + NT * i] =
+            cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(k1) * c) & Pmask, p.lfBig));
+        if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+      }
     }
   }
 }
