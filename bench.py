@@ -266,7 +266,8 @@ def side_config(key, dev, stream, peak, reps=20):
     gbs = w.bytes_alg(w.batch) / (ms / 1e3) / 1e9
     res = {"workload": f"config {w.key}: batch {w.batch} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
            "method": p.method, "kernel": kern, "ms_per_step": ms, "value": w.batch * w.m / (ms / 1e3),
-           "unit": "complex points/s", "hbm_gbs": gbs, "hbm_frac": gbs / peak, "reps": reps}
+           "unit": "complex points/s", "hbm_gbs": gbs, "hbm_frac": gbs / peak, "reps": reps,
+           "traffic": profiled_traffic(key, p.method), "bytes_alg": w.bytes_alg(w.batch)}
     del x, out
     torch.cuda.empty_cache()
     return res

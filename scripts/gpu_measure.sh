@@ -9,7 +9,7 @@ timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?" >> gpurun_out/bench_$TAG.err
 timeout 600 python bench.py --impl reference --steps 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
-CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alt"
+CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-alt --no-other-configs"
 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo done
