@@ -35,6 +35,9 @@
 #ifndef ASX_AFL_LAG
 #define ASX_AFL_LAG 0  // (ASX_AFL_OUT 1) team 1 starts a signal after team 0's S1 butterflies
 #endif
+#ifndef ASX_AFL_DEFER
+#define ASX_AFL_DEFER 1  // (ASX_AFL_OUT 0) write signal u-1's bins after signal u's S1 instead of behind a CTA barrier
+#endif
 #ifndef ASX_AFL_DBG
 #define ASX_AFL_DBG 0  // timing experiments only (wrong results): 1 no output, 2 no E1, 4 no E2, 8 no twiddle image
 #endif
@@ -101,13 +104,30 @@ struct AflCtx {
   uint64_t *full, *consumed, *war, *lag;
   uint32_t tbase;
   int t;
+  double2* xb0;      // ASX_AFL_DEFER: both teams' buffers (the parked bins)
+  uint64_t* parked;  // ASX_AFL_DEFER: every warp has parked its bins
 };
+
+// X[e], e = c + 2d for the parked bins of signal u: contiguous across the
+// warp (full 32-byte sectors; residue c = e & 1 comes from team c's buffer)
+__device__ __forceinline__ void afl_copyout(const KParams& p, const double2* xb0, int u, int tid) {
+  using L = AfftLocal;
+  using C = double2;
+  C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+  const bool full_row = p.m >= L::P;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int e = tid + L::NTH * j, c = e & 1, d = e >> 1;
+    const C val = xb0[c * L::XB + L::out_pos(c, d & 15, (d >> 4) & 15, d >> 8)];
+    if (full_row || e < p.m) X[e] = val;
+  }
+}
 
 // One signal's residue CR on this team (t = team-local thread), up to the
 // parked outputs.
 template <int CR>
 __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, int u, int it, int stride,
-                                            bool live, uint32_t& phase, uint32_t xcnt) {
+                                            bool live, uint32_t& phase, uint32_t xcnt, bool live_prev) {
   using L = AfftLocal;
   using C = double2;
   const int t = cx.t, n0 = t & 15, hi = t >> 4;
@@ -135,6 +155,14 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   if (ASX_AFL_OUT == 1 && ASX_AFL_LAG && CR == 0) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(cx.lag);
+  }
+  if (ASX_AFL_OUT == 0 && ASX_AFL_DEFER && xcnt) {
+    // the previous signal's bins, parked by both teams long ago: write them now,
+    // between this signal's butterflies and its first exchange
+    mbar_wait(cx.parked, (xcnt - 1) & 1);
+    if (live_prev && !(ASX_AFL_DBG & 1)) afl_copyout(p, cx.xb0, u - stride, threadIdx.x);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
   }
   // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's output reads
   if (xcnt) mbar_wait(cx.war, (xcnt - 1) & 1);
@@ -179,6 +207,10 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   } else if (v[0].x == 12345.678) {
     xb[0] = v[1];
   }
+  if (ASX_AFL_OUT == 0 && ASX_AFL_DEFER) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.parked);
+  }
   if constexpr (ASX_AFL_OUT == 1) {
     asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");  // this team's bins parked
     if (live && !(ASX_AFL_DBG & 1)) {
@@ -215,6 +247,8 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
   cx.consumed = bars + 1;
   cx.war = bars + 2 + (ASX_AFL_OUT ? team : 0);
   cx.lag = bars + 4;
+  cx.parked = bars + 4;  // (only one of lag / parked is in use)
+  cx.xb0 = xb0;
   cx.t = tid & 255;
   const int stride = int(gridDim.x);
   int u = int(blockIdx.x);
@@ -225,7 +259,7 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
     mbar_init(cx.consumed, L::NTH / 32);
     mbar_init(bars + 2, (ASX_AFL_OUT ? L::TNT : L::NTH) / 32);
     mbar_init(bars + 3, L::TNT / 32);
-    mbar_init(bars + 4, L::TNT / 32);
+    mbar_init(bars + 4, (ASX_AFL_OUT == 0 && ASX_AFL_DEFER ? L::NTH : L::TNT) / 32);
     fence_mbar_init();
     if (u < batch) {  // first row in flight while the twiddles go to tensor memory
       mbar_expect_tx(cx.full, (uint32_t)L::ROW_BYTES);
@@ -261,12 +295,13 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
 #pragma unroll 1
   for (int it = 0; it < iters; ++it, u += stride) {
     const bool live = u < batch;
+    const bool live_prev = u - stride < batch;
     if (team == 0)
-      afl_residue<0>(p, cx, u, it, stride, live, phase, xcnt);
+      afl_residue<0>(p, cx, u, it, stride, live, phase, xcnt, live_prev);
     else
-      afl_residue<1>(p, cx, u, it, stride, live, phase, xcnt);
-    if (ASX_AFL_OUT == 0) __syncthreads();  // both residues parked
-    if (ASX_AFL_OUT == 0 && live && !(ASX_AFL_DBG & 1)) {
+      afl_residue<1>(p, cx, u, it, stride, live, phase, xcnt, live_prev);
+    if (ASX_AFL_OUT == 0 && !ASX_AFL_DEFER) __syncthreads();  // both residues parked
+    if (ASX_AFL_OUT == 0 && !ASX_AFL_DEFER && live && !(ASX_AFL_DBG & 1)) {
       // X[e], e = c + 2d: contiguous across the warp, residue c = e & 1
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
       const bool full_row = p.m >= L::P;
@@ -277,11 +312,16 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
         if (full_row || e < p.m) X[e] = val;
       }
     }
-    if (ASX_AFL_OUT == 0) {
+    if (ASX_AFL_OUT == 0 && !ASX_AFL_DEFER) {
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(cx.war);
     }
     ++xcnt;
+  }
+  if (ASX_AFL_OUT == 0 && ASX_AFL_DEFER && xcnt) {
+    const int u_last = u - stride;
+    mbar_wait(cx.parked, (xcnt - 1) & 1);
+    if (u_last < batch && !(ASX_AFL_DBG & 1)) afl_copyout(p, xb0, u_last, tid);
   }
   tmem_fence_before();
   __syncthreads();
