@@ -1,0 +1,316 @@
+// asx_chirp_local128.cuh — chirp-z α-DFT for P = 8192 complex128 with
+// group-local exchanges (BASELINE config 1b: N = M = 4096, α = 1/10, and any
+// complex128 chirp plan with 2N, 2M <= 8192).
+//
+// The same mathematics and the same forward-DIF / transposed-inverse scheme
+// as k_chirp_local (asx_chirp_local.cuh), re-factored for
+// 16-byte elements at 512 threads x 16 values (one signal per SM):
+//
+//   P1  radix-16 DIF over y[t + 512 i] (upper half zero), × W_8192^{t k1}
+//   G1  CTA-wide exchange: sub-problem k1 (512 points) -> warp k1
+//   P2  8 radix-2 DIF butterflies per thread over (n', n' + 256),
+//       × W_512^{n'} on the odd half                -> two 256-point halves
+//   L1  exchange inside the warp (every thread rewrites the slots it read)
+//   P3  radix-16 DIF over n'' = l + 16 i'' in the half-warp, × W_256^{l k3}
+//   L2  exchange inside the half-warp (padded 17)
+//   P4  radix-16 -> Y[f], f = k1 + 16 k2 + 32 k3 + 512 k4;  × H[f]; conj
+//   Q1..Q4 = P4ᵀ..P1ᵀ on the same thread <-> data map, ending in the io layout
+//
+// Per signal: 2 CTA-wide exchanges (the Stockham engine needs 6 at P = 8192,
+// R = 16: passes 2 x 16 x 16 x 16), 4 warp-local ones.  Tensor memory holds
+// per thread H (16 values in this thread's spectrum order), the chirp
+// (8 values) and the exact P1 / P2 twiddle seeds: 124 of 128 columns.
+#pragma once
+
+#include "asx_chirp_local.cuh"
+
+namespace asx {
+
+struct ChirpLocal128 {
+  static constexpr int P = 8192, NT = 512;
+  static constexpr int SUBR = 272;        // one 256-point half (+16 pad: the L2 layout l + 17 k3 fits)
+  static constexpr int REG = 2 * SUBR;    // one 512-point sub-problem (warp region)
+  static constexpr int XB = 16 * REG;     // exchange buffer (complex128 elements)
+  static constexpr int T3S = 17;          // T3 row stride: conflict-free 16 B reads
+  static constexpr int T3N = 16 * T3S;    // W_256^{l k3}, row l, column k3
+  static constexpr int CPT = 128;         // TMEM columns per thread: H 64 | chirp 32 | P1 seeds 24 | W_512^j 4
+  __host__ __device__ static constexpr int pos(int n) { return n + (n >> 8) * (SUBR - 256); }  // n < 512
+  __host__ __device__ static size_t stage_off() { return align_up(size_t(XB) * sizeof(double2), 128); }
+  __host__ __device__ static size_t tab_off(size_t row_bytes, bool staged) {
+    return stage_off() + (staged ? align_up(row_bytes, 128) : 0);
+  }
+  __host__ __device__ static size_t bar_off(size_t row_bytes, bool staged) {
+    return align_up(tab_off(row_bytes, staged) + size_t(T3N) * sizeof(double2), 16);
+  }
+  __host__ __device__ static size_t total(size_t row_bytes, bool staged) {
+    return bar_off(row_bytes, staged) + 2 * sizeof(uint64_t) + 16;  // stage mbar, WAR mbar, TMEM slot
+  }
+};
+
+// 4 consecutive complex128 values (16 TMEM columns) of this thread's lane
+__device__ __forceinline__ void tm_ld4c(uint32_t taddr, double2 (&out)[4]) {
+  uint32_t w[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+        "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out[k] = words_to_c(&w[4 * k], (double2*)nullptr);
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
+  static_assert(sizeof(Real) == 8, "complex128 kernel");
+  using C = double2;
+  using L = ChirpLocal128;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* xb = reinterpret_cast<C*>(smraw);
+  const int t = threadIdx.x, warp = t >> 5, j = t & 31, h = j >> 4, l = j & 15;
+  const bool staged = p.staged != 0;
+  const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(Real) : sizeof(C));
+  unsigned char* stage = smraw + L::stage_off();
+  C* T3 = reinterpret_cast<C*>(smraw + L::tab_off(row_bytes, staged));
+  uint64_t* stbar = reinterpret_cast<uint64_t*>(smraw + L::bar_off(row_bytes, staged));
+  uint64_t* war = stbar + 1;
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(stbar + 2);
+
+  for (int e = t; e < L::T3N; e += L::NT) {
+    const int row = e / L::T3S, col = e % L::T3S;  // l, k3
+    T3[e] = exact_w<C>(col < 16 ? row * col : 0, 256);
+  }
+  const int stride = int(gridDim.x);
+  int u = int(blockIdx.x);
+  const int batch = int(p.batch);
+  const int iters = (batch + stride - 1) / stride;
+  if (t == 0) {
+    mbar_init(stbar, 1);
+    mbar_init(war, L::NT / 32);
+    fence_mbar_init();
+    if (staged && u < batch) {
+      mbar_expect_tx(stbar, (uint32_t)row_bytes);
+      tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * (row_bytes / p.n),
+                  (uint32_t)row_bytes, stbar);
+    }
+  }
+  const C* chirp = reinterpret_cast<const C*>(p.chirp);
+  const C* H = reinterpret_cast<const C*>(p.H);
+  if (warp == 0) tmem_alloc(&tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * L::CPT);
+  {
+    // H in this thread's spectrum order f = k1 + 16 k2 + 32 k3 + 512 k4 (k1 = warp, k2 = h, k3 = l)
+    const int fbase = warp + 16 * h + 32 * l;
+#pragma unroll
+    for (int k0 = 0; k0 < 16; k0 += 2) {
+      uint32_t w8[8];
+      c_to_words(__ldg(H + fbase + 512 * k0), &w8[0]);
+      c_to_words(__ldg(H + fbase + 512 * (k0 + 1)), &w8[4]);
+      tmem_st8(tbase + 4 * k0, w8);
+    }
+    // chirp[t + 512 i], i < 8 (input and output rows share the io layout)
+#pragma unroll
+    for (int i0 = 0; i0 < 8; i0 += 2) {
+      uint32_t w8[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int idx = t + 512 * (i0 + k);
+        c_to_words(idx < p.chirp_len ? __ldg(chirp + idx) : mk(0.0, 0.0), &w8[4 * k]);
+      }
+      tmem_st8(tbase + 64 + 4 * i0, w8);
+    }
+    // exact W_8192^{e t} for e = 1, 2, 3, 4, 8, 12 and W_512^j
+    const int es[8] = {1, 2, 3, 4, 8, 12, 0, 0};
+#pragma unroll
+    for (int q0 = 0; q0 < 8; q0 += 2) {
+      uint32_t w8[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int q = q0 + k;
+        const C w = q < 6 ? exact_w<C>((es[q] * t) & (L::P - 1), L::P) : (q == 6 ? exact_w<C>(j, 512) : mk(1.0, 0.0));
+        c_to_words(w, &w8[4 * k]);
+      }
+      tmem_st8(tbase + 96 + 4 * q0, w8);
+    }
+    tmem_wait_st();
+  }
+  __syncthreads();
+
+  // P1 / Q4: u[r] *= W^{t r} from exact W, W^2, W^3 and seeds W^4, W^8, W^12
+  auto tw_p1 = [&](C (&v)[16]) {
+    C w[8];
+    tm_ld4c(tbase + 96, reinterpret_cast<C(&)[4]>(w[0]));
+    tm_ld4c(tbase + 112, reinterpret_cast<C(&)[4]>(w[4]));
+    v[1] = cmul(v[1], w[0]);
+    v[2] = cmul(v[2], w[1]);
+    v[3] = cmul(v[3], w[2]);
+#pragma unroll
+    for (int a = 1; a < 4; ++a) {
+      const C w4a = w[2 + a];
+      v[4 * a] = cmul(v[4 * a], w4a);
+      v[4 * a + 1] = cmul(v[4 * a + 1], cmul(w4a, w[0]));
+      v[4 * a + 2] = cmul(v[4 * a + 2], cmul(w4a, w[1]));
+      v[4 * a + 3] = cmul(v[4 * a + 3], cmul(w4a, w[2]));
+    }
+  };
+  // P2 / Q3 twiddle of pair q: W_512^{j + 32 q} = W_512^j W_16^q
+  auto w512 = [&]() {
+    C w[4];
+    tm_ld4c(tbase + 112, w);
+    return w[2];
+  };
+  // P3 / Q2: v[k3] *= W_256^{l k3}
+  auto tw_p3 = [&](C (&v)[16]) {
+    const C* row = T3 + L::T3S * l;
+#pragma unroll
+    for (int k3 = 1; k3 < 16; ++k3) v[k3] = cmul(v[k3], row[k3]);
+  };
+  const bool fast_in = staged && !p.real_in && p.n >= L::P / 2;
+  const bool fast_out = p.m >= L::P / 2;
+  C* const rg = xb + warp * L::REG;  // this warp's sub-problem region
+  C* const sr = rg + h * L::SUBR;    // this half-warp's 256-point half
+  uint32_t phase = 0, xcnt = 0;
+
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it, u += stride) {
+    const bool live = u < batch;
+    const int64_t row_off = int64_t(u) * p.xs;
+    C v[16];
+    if (staged && live) {
+      mbar_wait(stbar, phase);
+      phase ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = mk(0.0, 0.0);
+#pragma unroll
+    for (int i0 = 0; i0 < 8; i0 += 4) {
+      C cw[4];
+      tm_ld4c(tbase + 64 + 4 * i0, cw);
+      if (fast_in && live) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[i0 + k] = cmul(reinterpret_cast<const C*>(stage)[t + 512 * (i0 + k)], cw[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int nn = t + 512 * (i0 + k);
+          if (live && nn < p.n) v[i0 + k] = cmul(load_row<C>(stage, p.x, row_off, nn, p.real_in, staged), cw[k]);
+        }
+      }
+    }
+    // ---- P1: radix-16 DIF (upper half zero), × W_8192^{t k1}
+    dft_reg<16>(v);
+    tw_p1(v);
+    // ---- G1: y_k1[t] -> region k1 (WAR: the previous signal's Q4 reads)
+    if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) xb[k1 * L::REG + L::pos(t)] = v[k1];
+    __syncthreads();  // G1 RAW; every thread has consumed the staged row
+    if (staged && t == 0 && u + stride < batch) {
+      fence_proxy_async();
+      mbar_expect_tx(stbar, (uint32_t)row_bytes);
+      tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * (row_bytes / p.n),
+                  (uint32_t)row_bytes, stbar);
+    }
+    // ---- P2: (a, b) = (y[n'], y[n' + 256]), n' = j + 32 q -> (a + b, (a - b) W_512^{n'})
+    {
+      const C wj = w512();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const C a = rg[j + 32 * q], b = rg[L::SUBR + j + 32 * q];
+        v[q] = cadd(a, b);
+        v[8 + q] = tw_const<16>(cmul(csub(a, b), wj), q);
+      }
+    }
+    // ---- L1: half k2 -> half-warp k2 (each thread rewrites the slots it read)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      rg[j + 32 * q] = v[q];
+      rg[L::SUBR + j + 32 * q] = v[8 + q];
+    }
+    __syncwarp();
+    // ---- P3: radix-16 DIF over n'' = l + 16 i'', × W_256^{l k3}
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = sr[l + 16 * i];
+    dft_reg<16>(v);
+    tw_p3(v);
+    __syncwarp();
+    // ---- L2 (half-warp): (l, k3) -> thread k3
+#pragma unroll
+    for (int k3 = 0; k3 < 16; ++k3) sr[l + 17 * k3] = v[k3];
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < 16; ++n) v[n] = sr[n + 17 * l];
+    // ---- P4: radix-16 -> Y[f], × H[f], conj
+    dft_reg<16>(v);
+#pragma unroll
+    for (int k0 = 0; k0 < 16; k0 += 4) {
+      C hw[4];
+      tm_ld4c(tbase + 4 * k0, hw);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k0 + k] = cconj(cmul(v[k0 + k], hw[k]));
+    }
+    // ---- inverse = conj(DFT(conj(.))): Q1 = P4ᵀ
+    dft_reg<16>(v);
+#pragma unroll
+    for (int n = 0; n < 16; ++n) sr[n + 17 * l] = v[n];  // L2ᵀ: the slots this thread read
+    __syncwarp();
+#pragma unroll
+    for (int k3 = 0; k3 < 16; ++k3) v[k3] = sr[l + 17 * k3];
+    // ---- Q2 = P3ᵀ
+    tw_p3(v);
+    dft_reg<16>(v);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sr[l + 16 * i] = v[i];  // L1ᵀ
+    __syncwarp();
+    // ---- Q3 = P2ᵀ: (A, B) -> (A + W B, A - W B) back to (n', n' + 256)
+    {
+      const C wj = w512();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const C A = rg[j + 32 * q];
+        const C WB = tw_const<16>(cmul(rg[L::SUBR + j + 32 * q], wj), q);
+        rg[j + 32 * q] = cadd(A, WB);
+        rg[L::SUBR + j + 32 * q] = csub(A, WB);
+      }
+    }
+    __syncthreads();  // G1ᵀ RAW
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
+    __syncwarp();
+    if ((t & 31) == 0) mbar_arrive(war);
+    ++xcnt;
+    // ---- Q4 = P1ᵀ: × W_8192^{t k1}, radix-16 -> X[t + 512 i], i < 8
+    tw_p1(v);
+    dft_reg<16>(v);
+    {
+      C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+#pragma unroll
+      for (int i0 = 0; i0 < 8; i0 += 4) {
+        C cw[4];
+        tm_ld4c(tbase + 64 + 4 * i0, cw);
+        if (fast_out && live) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) X[t + 512 * (i0 + k)] = cmul(cconj(v[i0 + k]), cw[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int mm = t + 512 * (i0 + k);
+            if (live && mm < p.m) X[mm] = cmul(cconj(v[i0 + k]), cw[k]);
+          }
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(tmem_slot, 512);
+}
+
+}  // namespace asx

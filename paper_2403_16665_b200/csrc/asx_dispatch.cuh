@@ -13,6 +13,7 @@
 #include "asx_afft_local.cuh"
 #include "asx_chirp2h.cuh"
 #include "asx_chirp_local.cuh"
+#include "asx_chirp_local128.cuh"
 #include "asx_large.cuh"
 
 namespace asx_host {
@@ -173,6 +174,35 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
       g_last_launch.block = AfftLocal::NTH;
       g_last_launch.smem = (int)AfftLocal::SMEM;
       g_last_launch.staged = 1;
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (KIND == KIND_CHIRP && sizeof(Real) == 8 && P == ChirpLocal128::P) {
+    // complex128 group-local chirp kernel (asx_chirp_local128.cuh): one CTA per SM
+    if (env.use_local && env.use_tmem && 2 * kp.m <= P && 2 * kp.n <= P && batch < (int64_t(1) << 31)) {
+      using CL = ChirpLocal128;
+      auto kl = k_chirp_local128<double>;
+      size_t smem_l = CL::total(row_bytes, kp.staged != 0);
+      if (smem_l > env.smem_optin) {
+        kp.staged = 0;
+        smem_l = CL::total(row_bytes, false);
+      }
+      static thread_local int cl_attr_for = -1;
+      int dev_l = 0;
+      cudaGetDevice(&dev_l);
+      if (cl_attr_for != dev_l) {
+        cudaError_t e = cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
+        if (e != cudaSuccess) return e;
+        cl_attr_for = dev_l;
+      }
+      const int64_t grid_l = std::min<int64_t>(batch, env.sms);
+      kp.batch = batch;
+      kl<<<(unsigned)grid_l, CL::NT, smem_l, st>>>(kp);
+      g_last_launch.tmem = 6;
+      g_last_launch.grid = (int)grid_l;
+      g_last_launch.block = CL::NT;
+      g_last_launch.smem = (int)smem_l;
+      g_last_launch.staged = kp.staged;
       return cudaGetLastError();
     }
   }
