@@ -24,6 +24,10 @@
 
 #include "asx_chirp_local.cuh"
 
+#ifndef ASX_CL128_SHFL
+#define ASX_CL128_SHFL 1  // L1 / L1ᵀ as lane-pair shuffles instead of a shared-memory round trip
+#endif
+
 namespace asx {
 
 struct ChirpLocal128 {
@@ -217,7 +221,21 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
                   (uint32_t)row_bytes, stbar);
     }
     // ---- P2: (a, b) = (y[n'], y[n' + 256]), n' = j + 32 q -> (a + b, (a - b) W_512^{n'})
-    {
+    if (ASX_CL128_SHFL) {
+      // L1 as a lane-pair swap: n' = l + 16 (h + 2q), so lane (h, l) already holds
+      // the i'' = h + 2q half of both 256-point halves; it keeps half k2 = h and
+      // trades the other with lane l + 16 (h ^ 1)
+      const C wj = w512();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const C a = rg[j + 32 * q], b = rg[L::SUBR + j + 32 * q];
+        const C A = cadd(a, b), B = tw_const<16>(cmul(csub(a, b), wj), q);
+        const C snd = h ? A : B;
+        const C rcv = mk(__shfl_xor_sync(0xffffffffu, snd.x, 16), __shfl_xor_sync(0xffffffffu, snd.y, 16));
+        v[2 * q] = h ? rcv : A;
+        v[2 * q + 1] = h ? B : rcv;
+      }
+    } else {
       const C wj = w512();
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -225,17 +243,17 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
         v[q] = cadd(a, b);
         v[8 + q] = tw_const<16>(cmul(csub(a, b), wj), q);
       }
-    }
-    // ---- L1: half k2 -> half-warp k2 (each thread rewrites the slots it read)
+      // ---- L1: half k2 -> half-warp k2 (each thread rewrites the slots it read)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      rg[j + 32 * q] = v[q];
-      rg[L::SUBR + j + 32 * q] = v[8 + q];
+      for (int q = 0; q < 8; ++q) {
+        rg[j + 32 * q] = v[q];
+        rg[L::SUBR + j + 32 * q] = v[8 + q];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = sr[l + 16 * i];
     }
-    __syncwarp();
     // ---- P3: radix-16 DIF over n'' = l + 16 i'', × W_256^{l k3}
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = sr[l + 16 * i];
     dft_reg<16>(v);
     tw_p3(v);
     __syncwarp();
@@ -264,12 +282,25 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
     // ---- Q2 = P3ᵀ
     tw_p3(v);
     dft_reg<16>(v);
-    __syncwarp();
+    if (ASX_CL128_SHFL) {
+      // ---- L1ᵀ (lane-pair swap) and Q3 = P2ᵀ: (A, B) -> (A + W B, A - W B) at (n', n' + 256);
+      // the shuffles order every lane's Q2 reads before the writes below
+      const C wj = w512();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) sr[l + 16 * i] = v[i];  // L1ᵀ
-    __syncwarp();
-    // ---- Q3 = P2ᵀ: (A, B) -> (A + W B, A - W B) back to (n', n' + 256)
-    {
+      for (int q = 0; q < 8; ++q) {
+        const C snd = h ? v[2 * q] : v[2 * q + 1];
+        const C rcv = mk(__shfl_xor_sync(0xffffffffu, snd.x, 16), __shfl_xor_sync(0xffffffffu, snd.y, 16));
+        const C A = h ? rcv : v[2 * q];
+        const C WB = tw_const<16>(cmul(h ? v[2 * q + 1] : rcv, wj), q);
+        rg[j + 32 * q] = cadd(A, WB);
+        rg[L::SUBR + j + 32 * q] = csub(A, WB);
+      }
+    } else {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) sr[l + 16 * i] = v[i];  // L1ᵀ
+      __syncwarp();
+      // ---- Q3 = P2ᵀ: (A, B) -> (A + W B, A - W B) back to (n', n' + 256)
       const C wj = w512();
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
