@@ -91,6 +91,7 @@ struct asx_plan_s {
   int large = 0;
   int64_t P1 = 0, P2 = 0;
   int lfBig = 0;
+  int row_local = 0;  // complex128 P2 = 8192: rows on k_large_rows_local, Ht stored permuted
   size_t off_twP1 = 0, off_twBig = 0, off_A = 0;
   // chirp "two halves" kernel (P = 2Q split into even/odd Q-point FFTs)
   int half = 0;
@@ -276,7 +277,7 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
       lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
       lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
       e = launch_large(dbl, p->P1, COL_FWD_SIGNAL, 0, 0, lp, st);
-      if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_MAIN, 1, lp, st);
+      if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, p->row_local ? ROW_MAIN_LOCAL : ROW_MAIN, 1, lp, st);
       if (e == cudaSuccess) e = launch_large(dbl, p->P1, COL_INV_OUT, 0, 0, lp, st);
     }
   } else {
@@ -588,6 +589,13 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
         lp.P2 = p->P2;
         e = launch_large(dbl, p->P1, COL_FWD_TABLE, 0, 0, lp, st);
         if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_SPECTRUM, 1, lp, st);
+        p->row_local = (dbl && p->P2 == ChirpLocal128::P && p->env.use_local && p->env.use_tmem) ? 1 : 0;
+        if (e == cudaSuccess && p->row_local) {
+          // Ht rows in k_large_rows_local's per-thread spectrum order (hbuf is free again)
+          k_permute_ht<<<4096, 256, 0, st>>>(static_cast<double2*>(hbuf),
+                                             reinterpret_cast<const double2*>(base + p->off_H), p->P1);
+          e = cudaMemcpyAsync(base + p->off_H, hbuf, es * chirp_P, cudaMemcpyDeviceToDevice, st);
+        }
         cudaFreeAsync(hbuf, st);
       }
     } else if ((e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), 2 * sizeof(double2) * p->P, st)) ==

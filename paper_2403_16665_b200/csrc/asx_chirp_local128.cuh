@@ -23,6 +23,7 @@
 #pragma once
 
 #include "asx_chirp_local.cuh"
+#include "asx_large.cuh"
 
 #ifndef ASX_CL128_SHFL
 #define ASX_CL128_SHFL 1  // L1 / L1ᵀ as lane-pair shuffles instead of a shared-memory round trip
@@ -336,6 +337,210 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
           }
         }
       }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc(tmem_slot, 512);
+}
+
+
+
+// ---------------------------------------------------------------------------
+// k_large_rows_local: the four-step path's fused row pass (asx_large.cuh KB,
+// BASELINE config 2: P = 2^23 = 1024 rows x 8192) on the same group-local
+// structure: per row k1, forward FFT_8192 (P1 .. P4, DIF) -> × Ht[k1][f] in
+// the per-thread spectrum order (the plan stores Ht permuted that way,
+// k_permute_ht) -> conj -> the transposed chain Q1 .. Q4 -> × W_P^{k1 c} back
+// into the row.  Persistent over rows, the next row of A and of Ht prefetched
+// into L2.  2 CTA-wide exchanges per row instead of the engine's 6.
+// ---------------------------------------------------------------------------
+struct RowsLocal {
+  using L = ChirpLocal128;
+  static constexpr size_t T3_OFF = align_up(size_t(L::XB) * sizeof(double2), 128);
+  static constexpr size_t BAR_OFF = align_up(T3_OFF + size_t(L::T3N) * sizeof(double2), 16);
+  static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) + 16;  // WAR mbar, TMEM slot
+  // position of spectrum bin f's value in the permuted Ht row: thread
+  // t = 32 k1' + 16 k2 + k3 holds f = k1' + 16 k2 + 32 k3 + 512 k4 at t + 512 k4
+  __host__ __device__ static constexpr int perm_src(int slot) {
+    return ((slot & 511) >> 5) + 16 * ((slot >> 4) & 1) + 32 * (slot & 15) + 512 * (slot >> 9);
+  }
+};
+
+// dst[r][slot] = src[r][perm_src(slot)] for r < rows (plan time)
+static __global__ void k_permute_ht(double2* __restrict__ dst, const double2* __restrict__ src, int64_t rows) {
+  const int64_t total = rows * 8192;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i >> 13;
+    const int slot = int(i & 8191);
+    dst[i] = src[(r << 13) + RowsLocal::perm_src(slot)];
+  }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
+  static_assert(sizeof(Real) == 8, "complex128 kernel");
+  using C = double2;
+  using L = ChirpLocal128;
+  using RL = RowsLocal;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  C* xb = reinterpret_cast<C*>(smraw);
+  C* T3 = reinterpret_cast<C*>(smraw + RL::T3_OFF);
+  uint64_t* war = reinterpret_cast<uint64_t*>(smraw + RL::BAR_OFF);
+  uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(war + 1);
+  const int t = threadIdx.x, warp = t >> 5, j = t & 31, h = j >> 4, l = j & 15;
+  const int rows = int(p.P / L::P);
+  const uint64_t Pmask = uint64_t(p.P - 1);
+  for (int e = t; e < L::T3N; e += L::NT) {
+    const int row = e / L::T3S, col = e % L::T3S;
+    T3[e] = exact_w<C>(col < 16 ? row * col : 0, 256);
+  }
+  if (t == 0) {
+    mbar_init(war, L::NT / 32);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = tmem_slot + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * L::CPT);
+  {
+    const int es[8] = {1, 2, 3, 4, 8, 12, 0, 0};
+#pragma unroll
+    for (int q0 = 0; q0 < 8; q0 += 2) {
+      uint32_t w8[8];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int q = q0 + k;
+        const C w = q < 6 ? exact_w<C>((es[q] * t) & (L::P - 1), L::P) : (q == 6 ? exact_w<C>(j, 512) : mk(1.0, 0.0));
+        c_to_words(w, &w8[4 * k]);
+      }
+      tmem_st8(tbase + 96 + 4 * q0, w8);
+    }
+    tmem_wait_st();
+  }
+  __syncthreads();
+  auto tw_p1 = [&](C (&v)[16]) {
+    C w[8];
+    tm_ld4c(tbase + 96, reinterpret_cast<C(&)[4]>(w[0]));
+    tm_ld4c(tbase + 112, reinterpret_cast<C(&)[4]>(w[4]));
+    v[1] = cmul(v[1], w[0]);
+    v[2] = cmul(v[2], w[1]);
+    v[3] = cmul(v[3], w[2]);
+#pragma unroll
+    for (int a = 1; a < 4; ++a) {
+      const C w4a = w[2 + a];
+      v[4 * a] = cmul(v[4 * a], w4a);
+      v[4 * a + 1] = cmul(v[4 * a + 1], cmul(w4a, w[0]));
+      v[4 * a + 2] = cmul(v[4 * a + 2], cmul(w4a, w[1]));
+      v[4 * a + 3] = cmul(v[4 * a + 3], cmul(w4a, w[2]));
+    }
+  };
+  auto w512 = [&]() {
+    C w[4];
+    tm_ld4c(tbase + 112, w);
+    return w[2];
+  };
+  auto tw_p3 = [&](C (&v)[16]) {
+    const C* row = T3 + L::T3S * l;
+#pragma unroll
+    for (int k3 = 1; k3 < 16; ++k3) v[k3] = cmul(v[k3], row[k3]);
+  };
+  C* const rg = xb + warp * L::REG;
+  C* const sr = rg + h * L::SUBR;
+  const C* Ht = reinterpret_cast<const C*>(p.Ht);
+  const C* twb = reinterpret_cast<const C*>(p.twBig);
+  uint32_t xcnt = 0;
+#pragma unroll 1
+  for (int k1 = blockIdx.x; k1 < rows; k1 += gridDim.x) {
+    if (t == 0 && k1 + int(gridDim.x) < rows) {
+      const int64_t nxt = int64_t(k1 + gridDim.x) * L::P;
+      prefetch_l2_bulk(reinterpret_cast<const C*>(p.A) + nxt, uint32_t(L::P * sizeof(C)));
+      prefetch_l2_bulk(Ht + nxt, uint32_t(L::P * sizeof(C)));
+    }
+    C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * L::P;
+    C v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = row[t + 512 * i];
+    // ---- P1: radix-16 DIF, × W_8192^{t k1'}
+    dft_reg<16>(v);
+    tw_p1(v);
+    if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xb[k * L::REG + L::pos(t)] = v[k];
+    __syncthreads();  // G1 RAW
+    // ---- P2 + L1 (lane-pair swap)
+    {
+      const C wj = w512();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const C a = rg[j + 32 * q], b = rg[L::SUBR + j + 32 * q];
+        const C A = cadd(a, b), B = tw_const<16>(cmul(csub(a, b), wj), q);
+        const C snd = h ? A : B;
+        const C rcv = mk(__shfl_xor_sync(0xffffffffu, snd.x, 16), __shfl_xor_sync(0xffffffffu, snd.y, 16));
+        v[2 * q] = h ? rcv : A;
+        v[2 * q + 1] = h ? B : rcv;
+      }
+    }
+    // ---- P3, L2, P4
+    dft_reg<16>(v);
+    tw_p3(v);
+    __syncwarp();
+#pragma unroll
+    for (int k3 = 0; k3 < 16; ++k3) sr[l + 17 * k3] = v[k3];
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < 16; ++n) v[n] = sr[n + 17 * l];
+    dft_reg<16>(v);
+    // ---- × Ht (permuted row: this thread's bins are contiguous across the CTA), conj
+    {
+      const C* hr = Ht + int64_t(k1) * L::P + t;
+#pragma unroll
+      for (int k0 = 0; k0 < 16; k0 += 8) {
+        C hw[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) hw[k] = __ldg(hr + 512 * (k0 + k));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k0 + k] = cconj(cmul(v[k0 + k], hw[k]));
+      }
+    }
+    // ---- Q1, L2ᵀ, Q2
+    dft_reg<16>(v);
+#pragma unroll
+    for (int n = 0; n < 16; ++n) sr[n + 17 * l] = v[n];
+    __syncwarp();
+#pragma unroll
+    for (int k3 = 0; k3 < 16; ++k3) v[k3] = sr[l + 17 * k3];
+    tw_p3(v);
+    dft_reg<16>(v);
+    // ---- L1ᵀ (lane-pair swap) + Q3
+    {
+      const C wj = w512();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const C snd = h ? v[2 * q] : v[2 * q + 1];
+        const C rcv = mk(__shfl_xor_sync(0xffffffffu, snd.x, 16), __shfl_xor_sync(0xffffffffu, snd.y, 16));
+        const C A = h ? rcv : v[2 * q];
+        const C WB = tw_const<16>(cmul(h ? v[2 * q + 1] : rcv, wj), q);
+        rg[j + 32 * q] = cadd(A, WB);
+        rg[L::SUBR + j + 32 * q] = csub(A, WB);
+      }
+    }
+    __syncthreads();  // G1ᵀ RAW
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = xb[k * L::REG + L::pos(t)];
+    __syncwarp();
+    if ((t & 31) == 0) mbar_arrive(war);
+    ++xcnt;
+    // ---- Q4 = P1ᵀ -> B[k1][c], c = t + 512 i, times W_P^{k1 c}
+    tw_p1(v);
+    dft_reg<16>(v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t c = uint64_t(t + 512 * i);
+      row[t + 512 * i] = cmul(v[i], tw_big(twb, (uint64_t(k1) * c) & Pmask, p.lfBig));
+      if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
     }
   }
   tmem_fence_before();

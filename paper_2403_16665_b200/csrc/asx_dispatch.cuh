@@ -370,6 +370,18 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
       cudaGetLastError();
     if (e == cudaSuccess) kern<<<(unsigned)std::min<int64_t>(P1, sms), G::NT, smem, st>>>(lp);
   };
+  if constexpr (sizeof(Real) == 8) {
+    if (mode == ROW_MAIN_LOCAL) {
+      auto kern = k_large_rows_local<double>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RowsLocal::SMEM);
+      int sms = 148, dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        cudaGetLastError();
+      if (e == cudaSuccess) kern<<<(unsigned)std::min<int64_t>(P1, sms), ChirpLocal128::NT, RowsLocal::SMEM, st>>>(lp);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
+  }
   if (mode == ROW_SPECTRUM)
     go(k_large_rows<Real, P2, G::NT, ROW_SPECTRUM>);
   else

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   }
 }
 
-enum { ROW_SPECTRUM = 0, ROW_MAIN = 1 };
+enum { ROW_SPECTRUM = 0, ROW_MAIN = 1, ROW_MAIN_LOCAL = 2 };  // 2: k_large_rows_local (asx_chirp_local128.cuh)
 
 __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
