@@ -45,7 +45,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the non-production methods")
     ap.add_argument("--no-other-configs", action="store_true",
-                    help="skip the untimed-in-headline side measurement of config 1a (alpha-FFT recursion)")
+                    help="skip the side measurements of configs 1a, 1b and 3 (not part of value)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target busy seconds per host core for the CPU baseline sample")
     return ap.parse_args()
@@ -120,6 +120,8 @@ def launched_kernel(method: str) -> str:
         return "k_chirp_local<float> (group-local exchanges, csrc/asx_chirp_local.cuh)"
     if method == "fft" and variant == 4:
         return "k_afft_local<double> (group-local alpha-FFT, csrc/asx_afft_local.cuh)"
+    if method == "chirp" and variant == 6:
+        return "k_chirp_local128<double> (group-local chirp-z, csrc/asx_chirp_local128.cuh)"
     if method == "direct":
         return "k_direct"
     kind = "afft" if method == "fft" else "chirp"
@@ -253,7 +255,7 @@ def side_config(key, dev, stream, peak, reps=20):
 
     w = WORKLOADS[key]
     x = generate_device(w, 0, w.batch, device=dev)
-    p = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, real_input=w.real, device=dev.index)
+    p = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, method="auto", real_input=w.real, device=dev.index)
     out = torch.empty((w.batch, w.m), dtype=getattr(torch, w.dtype), device=dev)
     for _ in range(3):
         p.execute(x, out=out)
@@ -391,12 +393,14 @@ def run_gpu(args):
                            "how": "concurrent pinned 512 MiB copies on two streams from one start event, best of 5",
                            "bound_ms": bound_s * 1e3, "frac": bound_s / e2e_s}
 
-    # side measurement (world 1 only, not part of `value`): the batched α-FFT
-    # recursion itself on config 1a, the one BASELINE config whose op count
-    # lets the α-FFT approach the HBM roofline
+    # side measurements (world 1 only, not part of `value`): the other batched
+    # BASELINE configs -- 1a (the α-FFT recursion itself, the one config whose
+    # op count lets it approach the HBM roofline), 1b and 3
     other = {}
-    if world == 1 and not args.no_other_configs and args.config != "1a":
-        other["1a"] = side_config("1a", dev, stream, peak)
+    if world == 1 and not args.no_other_configs:
+        for key in ("1a", "1b", "3"):
+            if key != args.config:
+                other[key] = side_config(key, dev, stream, peak)
 
     # untimed verification collective: per-rank checksums gathered over NCCL
     checks = gather_checksums(out, device=dev)
