@@ -15,9 +15,10 @@
 //   S2  radix-16 over n1 -> g1, × W_256^{n0 g1} (exact, tensor memory)
 //   E2  exchange inside the half-warp (__syncwarp): -> thread (g1, g0)
 //   S3  radix-16 over n0 -> g2; only g2 < 8 (d < N/2, i.e. m < N) is kept
-//   OUT both teams park their bins in their own half-warp regions, one CTA
-//       barrier, then all 512 threads write X[e] with e contiguous across the
-//       warp (full 32-byte sectors: the residues interleave as m = c + 2d)
+//   OUT both teams park their bins in their own half-warp regions; one signal
+//       later (between the next signal's S1 and E1, after a split-phase
+//       "parked" mbarrier) all 512 threads write X[e] with e contiguous across
+//       the warp (full 32-byte sectors: the residues interleave as m = c + 2d)
 //
 // Per residue: one team-wide and one half-warp exchange (the Stockham engine
 // needs three team-wide ones at R = 8), the α pre-twiddle folded into the
@@ -29,15 +30,6 @@
 
 #include "asx_kernels.cuh"
 
-#ifndef ASX_AFL_OUT
-#define ASX_AFL_OUT 0  // 0: CTA-wide copy-out (full sectors); 1: per-team copy-out (teams decoupled)
-#endif
-#ifndef ASX_AFL_LAG
-#define ASX_AFL_LAG 0  // (ASX_AFL_OUT 1) team 1 starts a signal after team 0's S1 butterflies
-#endif
-#ifndef ASX_AFL_DEFER
-#define ASX_AFL_DEFER 1  // (ASX_AFL_OUT 0) write signal u-1's bins after signal u's S1 instead of behind a CTA barrier
-#endif
 #ifndef ASX_AFL_DBG
 #define ASX_AFL_DBG 0  // timing experiments only (wrong results): 1 no output, 2 no E1, 4 no E2, 8 no twiddle image
 #endif
@@ -51,7 +43,7 @@ struct AfftLocal {
   static constexpr size_t STAGE_OFF = size_t(2) * XB * sizeof(double2);
   static constexpr size_t ROW_BYTES = size_t(P) * sizeof(double2);
   static constexpr size_t BAR_OFF = STAGE_OFF + ROW_BYTES;
-  static constexpr size_t SMEM = BAR_OFF + 5 * sizeof(uint64_t) + 16;  // full, consumed, war[2], lag, TMEM slot
+  static constexpr size_t SMEM = BAR_OFF + 5 * sizeof(uint64_t) + 16;  // full, consumed, war, -, parked, TMEM slot
   static constexpr int CPT = 128;       // TMEM columns per thread: S1 twiddles 16 x 4 | S2 twiddles 16 x 4
   static constexpr int IMG_ELEMS = 32 * NTH;  // twiddle image: [j < 32][thread < 512] complex128
   // parked output bin (g1, g2) of half-warp region hi of team c (conflict-free both ways)
@@ -101,11 +93,11 @@ __device__ __forceinline__ void afl_twiddle(double2 (&v)[16], uint32_t col) {
 struct AflCtx {
   double2* xb;  // this team's exchange buffer
   const unsigned char* stage;
-  uint64_t *full, *consumed, *war, *lag;
+  uint64_t *full, *consumed, *war;
   uint32_t tbase;
   int t;
-  double2* xb0;      // ASX_AFL_DEFER: both teams' buffers (the parked bins)
-  uint64_t* parked;  // ASX_AFL_DEFER: every warp has parked its bins
+  double2* xb0;      // both teams' buffers (the parked bins)
+  uint64_t* parked;  // every warp has parked its bins
 };
 
 // X[e], e = c + 2d for the parked bins of signal u: contiguous across the
@@ -132,7 +124,6 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   using C = double2;
   const int t = cx.t, n0 = t & 15, hi = t >> 4;
   C v[16];
-  if (ASX_AFL_OUT == 1 && ASX_AFL_LAG && CR == 1) mbar_wait(cx.lag, it & 1);
   if (live) {
     mbar_wait(cx.full, phase);
     phase ^= 1;
@@ -152,11 +143,7 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   }
   dft_reg<16>(v);
   afl_twiddle<CR == 0 ? 1 : 0>(v, cx.tbase);
-  if (ASX_AFL_OUT == 1 && ASX_AFL_LAG && CR == 0) {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.lag);
-  }
-  if (ASX_AFL_OUT == 0 && ASX_AFL_DEFER && xcnt) {
+  if (xcnt) {
     // the previous signal's bins, parked by both teams long ago: write them now,
     // between this signal's butterflies and its first exchange
     mbar_wait(cx.parked, (xcnt - 1) & 1);
@@ -203,28 +190,12 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   dft_reg<16>(v);
   if (!(ASX_AFL_DBG & 1)) {
 #pragma unroll
-    for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(ASX_AFL_OUT ? 0 : CR, hi, n0, g2)] = v[g2];
+    for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(CR, hi, n0, g2)] = v[g2];
   } else if (v[0].x == 12345.678) {
     xb[0] = v[1];
   }
-  if (ASX_AFL_OUT == 0 && ASX_AFL_DEFER) {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.parked);
-  }
-  if constexpr (ASX_AFL_OUT == 1) {
-    asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");  // this team's bins parked
-    if (live && !(ASX_AFL_DBG & 1)) {
-      C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int d = t + 256 * j, mm = CR + 2 * d;
-        const C val = xb[L::out_pos(0, d & 15, (d >> 4) & 15, d >> 8)];
-        if (p.m >= L::P || mm < p.m) X[mm] = val;
-      }
-    }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
-  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(cx.parked);
 }
 
 // Launch: grid <= #SMs, NTH threads, AfftLocal::SMEM dynamic shared memory.
@@ -245,9 +216,8 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
   cx.stage = smraw + L::STAGE_OFF;
   cx.full = bars;
   cx.consumed = bars + 1;
-  cx.war = bars + 2 + (ASX_AFL_OUT ? team : 0);
-  cx.lag = bars + 4;
-  cx.parked = bars + 4;  // (only one of lag / parked is in use)
+  cx.war = bars + 2;
+  cx.parked = bars + 4;
   cx.xb0 = xb0;
   cx.t = tid & 255;
   const int stride = int(gridDim.x);
@@ -257,9 +227,8 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
   if (tid == 0) {
     mbar_init(cx.full, 1);
     mbar_init(cx.consumed, L::NTH / 32);
-    mbar_init(bars + 2, (ASX_AFL_OUT ? L::TNT : L::NTH) / 32);
-    mbar_init(bars + 3, L::TNT / 32);
-    mbar_init(bars + 4, (ASX_AFL_OUT == 0 && ASX_AFL_DEFER ? L::NTH : L::TNT) / 32);
+    mbar_init(cx.war, L::NTH / 32);
+    mbar_init(cx.parked, L::NTH / 32);
     fence_mbar_init();
     if (u < batch) {  // first row in flight while the twiddles go to tensor memory
       mbar_expect_tx(cx.full, (uint32_t)L::ROW_BYTES);
@@ -300,25 +269,9 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
       afl_residue<0>(p, cx, u, it, stride, live, phase, xcnt, live_prev);
     else
       afl_residue<1>(p, cx, u, it, stride, live, phase, xcnt, live_prev);
-    if (ASX_AFL_OUT == 0 && !ASX_AFL_DEFER) __syncthreads();  // both residues parked
-    if (ASX_AFL_OUT == 0 && !ASX_AFL_DEFER && live && !(ASX_AFL_DBG & 1)) {
-      // X[e], e = c + 2d: contiguous across the warp, residue c = e & 1
-      C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
-      const bool full_row = p.m >= L::P;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int e = tid + L::NTH * j, c = e & 1, d = e >> 1;
-        const C val = xb0[c * L::XB + L::out_pos(c, d & 15, (d >> 4) & 15, d >> 8)];
-        if (full_row || e < p.m) X[e] = val;
-      }
-    }
-    if (ASX_AFL_OUT == 0 && !ASX_AFL_DEFER) {
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(cx.war);
-    }
     ++xcnt;
   }
-  if (ASX_AFL_OUT == 0 && ASX_AFL_DEFER && xcnt) {
+  if (xcnt) {  // the last signal's bins
     const int u_last = u - stride;
     mbar_wait(cx.parked, (xcnt - 1) & 1);
     if (u_last < batch && !(ASX_AFL_DBG & 1)) afl_copyout(p, xb0, u_last, tid);
