@@ -224,7 +224,14 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
   kp.Xs = Xs;
   kp.batch = batch;
   cudaError_t e = cudaSuccess;
-  if (p->method == ASX_DIRECT) {
+  if (p->method == ASX_DIRECT && batch <= kDirectSmallBatch) {
+    const unsigned grid = (unsigned)((p->m + 1) / 2);  // 4 warps per bin, 2 bins per CTA
+    if (p->dtype == ASX_C64)
+      k_direct_small<float><<<grid, 256, 0, st>>>(kp);
+    else
+      k_direct_small<double><<<grid, 256, 0, st>>>(kp);
+    e = cudaGetLastError();
+  } else if (p->method == ASX_DIRECT) {
     const int64_t gy = (batch + 63) / 64, gx = (p->m + 63) / 64;
     if (gy > 65535) {
       // grid.y limit: walk the batch in slabs of 65535*64 signals
@@ -436,6 +443,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     p->env.use_split = (no_split && no_split[0] == '1') ? 0 : 1;
     const char* no_afl = std::getenv("ASX_NO_AFFT_LOCAL");
     p->env.use_afl = (no_afl && no_afl[0] == '1') ? 0 : 1;
+    const char* no_rs = std::getenv("ASX_NO_RSPLIT");
+    p->env.use_rsplit = (no_rs && no_rs[0] == '1') ? 0 : 1;
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && v > 0) p->env.sms = v;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)

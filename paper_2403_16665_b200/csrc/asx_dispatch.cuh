@@ -26,6 +26,7 @@ struct LaunchEnv {
   int use_local = 1; // P = 16384 complex64 chirp on k_chirp_local (env ASX_NO_LOCAL=1 disables)
   int use_split = 1; // α-FFT residues split over two teams sharing a staged row (env ASX_NO_SPLIT=1 disables)
   int use_afl = 1;   // complex128 N = 4096, α = 1/2 α-FFT on k_afft_local (env ASX_NO_AFFT_LOCAL=1 disables)
+  int use_rsplit = 1; // small α-FFT batches: one team per (signal, residue) (env ASX_NO_RSPLIT=1 disables)
 };
 
 // Shape of the most recent launch on this thread (asx_last_launch, for
@@ -250,7 +251,17 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
     }
   }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const int64_t need = (batch + G::TPB - 1) / G::TPB;
+  bool rsplit = false;
+  int64_t units = batch;
+  if constexpr (KIND == KIND_AFFT && KR == 1) {
+    // fewer signals than resident teams: one (signal, residue) pair per team
+    // instead of one signal, so a single signal's r residues run in parallel
+    if (env.use_rsplit && kp.r > 1 && batch < int64_t(env.sms) * per_sm * G::TPB && batch * kp.r < (int64_t(1) << 31)) {
+      rsplit = true;
+      units = batch * kp.r;
+    }
+  }
+  const int64_t need = (units + G::TPB - 1) / G::TPB;
   const int64_t grid = std::min<int64_t>(need, int64_t(env.sms) * per_sm);
   kp.batch = batch;
   int tm_used = 0;
@@ -272,7 +283,21 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
       tm_used = 1;
     }
   }
+  if constexpr (KIND == KIND_AFFT && KR == 1) {
+    if (rsplit) {
+      auto kern_rs = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR, false, true>;
+      static thread_local int rs_attr_for = -1;
+      if (rs_attr_for != dev) {
+        cudaError_t e = cudaFuncSetAttribute(kern_rs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
+        if (e != cudaSuccess) return e;
+        rs_attr_for = dev;
+      }
+      kern_rs<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
+      tm_used = -1;
+    }
+  }
   if (!tm_used) kern<<<(unsigned)grid, G::NT * G::TPB, smem, st>>>(kp);
+  if (tm_used < 0) tm_used = 0;
   g_last_launch.tmem = tm_used;
   g_last_launch.grid = (int)grid;
   g_last_launch.block = G::NT * G::TPB;

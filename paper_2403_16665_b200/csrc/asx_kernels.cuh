@@ -147,7 +147,10 @@ struct TmemCfg {
 // SPLIT (α-FFT only): the TPB teams of a CTA share ONE signal and split its
 // r output residues (team j takes c = j, j + TPB, ...); one TMA-staged row
 // serves them all, so a CTA of TPB teams keeps staging at full occupancy.
-template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1, bool SPLIT = false>
+// RS (α-FFT, small batches): the work unit is one (signal, residue) pair
+// instead of a signal, so one signal's r residues run on r teams at once.
+template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1, bool SPLIT = false,
+          bool RS = false>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   static_assert(!SPLIT || (KIND == 0 && NT > 32), "SPLIT: alpha-FFT with CTA-wide team barriers");
   constexpr bool TS = TM && KIND == KIND_CHIRP;  // last-pass twiddle seeds in TMEM too
@@ -182,7 +185,12 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   const int stride = int(gridDim.x) * SIG_PER_CTA;
   int u = int(blockIdx.x) * SIG_PER_CTA + (SPLIT ? 0 : team);
   const bool stage_owner = t == 0 && (!SPLIT || team == 0);
-  const int batch = int(p.batch);
+  // work units: signals, or (signal, residue) pairs when rsplit (small batches:
+  // the r residues of one signal run on r teams instead of one after another)
+  constexpr bool rs = KIND == KIND_AFFT && !SPLIT && RS;
+  const int nres = rs ? int(p.r) : 1;
+  const int batch = rs ? int(p.batch) * nres : int(p.batch);
+  auto sig = [&](int unit) { return rs ? unit / nres : unit; };
   const int iters = (batch + stride - 1) / stride;
   if (staged && stage_owner) {
     mbar_init(bar, 1);
@@ -193,7 +201,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   __syncthreads();
   if (staged && stage_owner && u < batch) {
     mbar_expect_tx(bar, (uint32_t)row_bytes);
-    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(u) * p.xs * (row_bytes / p.n),
+    tma_load_1d(stage, static_cast<const unsigned char*>(p.x) + int64_t(sig(u)) * p.xs * (row_bytes / p.n),
                 (uint32_t)row_bytes, bar);
   }
   uint32_t phase = 0;
@@ -248,7 +256,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
 #pragma unroll 1
   for (int it = 0; it < iters; ++it, u += stride) {
     const bool live = u < batch;
-    const int64_t row_off = int64_t(u) * p.xs;
+    const int64_t row_off = int64_t(sig(u)) * p.xs;
     if constexpr (KIND == KIND_CHIRP) {
       C v[R];
       if (staged && live) {
@@ -329,7 +337,9 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
       // KR output residues at a time: their transforms share twiddles and
       // barriers and interleave in the pipeline (ILP)
       // uniform trip count over the CTA (the team barriers are CTA-wide)
-      for (int cb = 0; cb < p.r; cb += KR * (SPLIT ? TPB : 1)) {
+      const int cbeg = rs ? u % nres : 0;
+      const int64_t cend = rs ? int64_t(cbeg + 1) : p.r;
+      for (int cb = cbeg; cb < cend; cb += KR * (SPLIT ? TPB : 1)) {
         const int c0 = cb + (SPLIT ? team * KR : 0);
         C v[KR][R];
 #pragma unroll
@@ -358,7 +368,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
             v[k][i] = val;
           }
         }
-        if (staged && cb + KR * (SPLIT ? TPB : 1) >= p.r) {
+        if (staged && cb + KR * (SPLIT ? TPB : 1) >= cend) {
           if constexpr (SPLIT)
             __syncthreads();  // every team has consumed the shared row
           else
@@ -367,13 +377,13 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
             fence_proxy_async();
             mbar_expect_tx(bar, (uint32_t)row_bytes);
             tma_load_1d(stage,
-                        static_cast<const unsigned char*>(p.x) + int64_t(u + stride) * p.xs * (row_bytes / p.n),
+                        static_cast<const unsigned char*>(p.x) + int64_t(sig(u + stride)) * p.xs * (row_bytes / p.n),
                         (uint32_t)row_bytes, bar);
           }
         }
         E::template run<KR>(v, fbuf, t, tr, xs);
         if (live) {
-          C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
+          C* X = reinterpret_cast<C*>(p.X) + int64_t(sig(u)) * p.Xs;
           const int64_t period = p.r * P;
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
@@ -460,6 +470,60 @@ __global__ void __launch_bounds__(256) k_direct(KParams p) {
       const int64_t mm = m0 + tx + 16 * j;
       if (mm < p.m) X[bb * p.Xs + mm] = acc[i][j];
     }
+  }
+}
+
+// Direct α-DFT for a handful of signals (batch <= kDirectSmallBatch): a
+// matrix-vector product per signal.  Four warps share one output bin m, each
+// streaming a quarter of row m of W (coalesced, lanes over n) and reusing it
+// for every signal of the batch; partial sums meet in shared memory.  The
+// 64-signal tile of k_direct would leave 63/64 of its work idle at batch 1
+// (config 0: 0.275 ms).
+constexpr int kDirectSmallBatch = 8;
+
+template <typename Real>
+__global__ void __launch_bounds__(256) k_direct_small(KParams p) {
+  using C = typename CT<Real>::T;
+  constexpr int NB = kDirectSmallBatch, WPB = 4;  // warps per bin
+  __shared__ C part[8][NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = warp % WPB;
+  const int64_t mm = int64_t(blockIdx.x) * (8 / WPB) + warp / WPB;
+  const int nb = int(p.batch);
+  C acc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) acc[b] = mk(Real(0), Real(0));
+  if (mm < p.m) {
+    const C* W = reinterpret_cast<const C*>(p.W) + mm * p.n;
+    const int64_t k0 = (p.n * q) / WPB, k1 = (p.n * (q + 1)) / WPB;
+#pragma unroll 4
+    for (int64_t k = k0 + lane; k < k1; k += 32) {
+      const C w = __ldg(W + k);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (b < nb) {
+          const C xv = load_in<C>(p.x, int64_t(b) * p.xs + k, p.real_in);
+          acc[b].x = fma(xv.x, w.x, fma(-xv.y, w.y, acc[b].x));
+          acc[b].y = fma(xv.x, w.y, fma(xv.y, w.x, acc[b].y));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    Real ax = acc[b].x, ay = acc[b].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ax += __shfl_xor_sync(0xffffffffu, ax, o);
+      ay += __shfl_xor_sync(0xffffffffu, ay, o);
+    }
+    if (lane == 0) part[warp][b] = mk(ax, ay);
+  }
+  __syncthreads();
+  if (q == 0 && lane < nb && mm < p.m) {
+    C s = part[warp][lane];
+#pragma unroll
+    for (int i = 1; i < WPB; ++i) s = cadd(s, part[warp + i][lane]);
+    reinterpret_cast<C*>(p.X)[int64_t(lane) * p.Xs + mm] = s;
   }
 }
 
