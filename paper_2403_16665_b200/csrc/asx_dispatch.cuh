@@ -342,10 +342,18 @@ cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t batch, c
 template <typename Real, int P1>
 cudaError_t launch_cols(int mode, const LParams& lp, cudaStream_t st) {
   using G = ColCfg<Real, P1>;
-  const unsigned grid = (unsigned)(lp.P2 / kColTile);
+  const int64_t tiles = lp.P2 / kColTile;
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kern) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+    // persistent: as many CTAs as fit on the device at once
+    int per_sm = 0, sms = 148, dev = 0;
+    if (e == cudaSuccess && (cudaGetDevice(&dev) != cudaSuccess ||
+                             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+                             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT * kColTile, G::SMEM) !=
+                                 cudaSuccess))
+      cudaGetLastError();
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, int64_t(sms) * std::max(per_sm, 1));
     if (e == cudaSuccess) kern<<<grid, G::NT * kColTile, G::SMEM, st>>>(lp);
   };
   if (mode == COL_FWD_SIGNAL)

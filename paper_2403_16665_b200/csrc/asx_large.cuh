@@ -85,62 +85,69 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   C* smbase = reinterpret_cast<C*>(smraw);
   const int team = threadIdx.x / NT, t = threadIdx.x % NT;
   C* sm = smbase + team * CS;
-  const int col0 = blockIdx.x * kColTile;
   C* tabp = smbase + kColTile * CS;
   const typename E::TwRegs tr = E::make_tw(t, reinterpret_cast<const C*>(p.twP1), tabp, threadIdx.x, THREADS);
   typename E::XSync xs;
   E::xs_init(xs, reinterpret_cast<uint64_t*>(tabp + E::TAB_ELEMS + (E::TAB_ELEMS & 1)), THREADS);
 
-  // ---- gather the 8-column tile: 8 threads per row, rows strided ----
-  {
-    const int tau = threadIdx.x & (kColTile - 1);
-    for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
-      const int64_t idx = int64_t(row) * P2 + col0 + tau;  // element index
-      C val = mk(Real(0), Real(0));
-      if constexpr (MODE == COL_FWD_SIGNAL) {
-        if (idx < p.n) {  // y[n] = x[n] * chirp[n], zero past N
-          const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(p.x) + idx), Real(0))
-                                 : __ldg(reinterpret_cast<const C*>(p.x) + idx);
-          val = cmul(xv, __ldg(reinterpret_cast<const C*>(p.chirp) + idx));
+  // persistent over column tiles: the per-CTA twiddle setup (make_tw, FP64
+  // sincospi seeds) is paid once per CTA instead of once per tile
+  const int ntiles = int(P2 / kColTile);
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int col0 = tile * kColTile;
+    __syncthreads();  // the previous tile's write-out reads of smbase are done
+    // ---- gather the column tile: kColTile threads per row, rows strided ----
+    {
+      const int tau = threadIdx.x & (kColTile - 1);
+      for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
+        const int64_t idx = int64_t(row) * P2 + col0 + tau;  // element index
+        C val = mk(Real(0), Real(0));
+        if constexpr (MODE == COL_FWD_SIGNAL) {
+          if (idx < p.n) {  // y[n] = x[n] * chirp[n], zero past N
+            const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(p.x) + idx), Real(0))
+                                   : __ldg(reinterpret_cast<const C*>(p.x) + idx);
+            val = cmul(xv, __ldg(reinterpret_cast<const C*>(p.chirp) + idx));
+          }
+        } else if constexpr (MODE == COL_FWD_TABLE) {
+          val = __ldg(reinterpret_cast<const C*>(p.h) + idx);
+        } else {
+          val = __ldg(reinterpret_cast<const C*>(p.A) + idx);  // B[k1][c], row = k1
         }
-      } else if constexpr (MODE == COL_FWD_TABLE) {
-        val = __ldg(reinterpret_cast<const C*>(p.h) + idx);
-      } else {
-        val = __ldg(reinterpret_cast<const C*>(p.A) + idx);  // B[k1][c], row = k1
+        smbase[tau * CS + E::pad(row)] = val;
       }
-      smbase[tau * CS + E::pad(row)] = val;
     }
-  }
-  __syncthreads();
-  C v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) v[i] = sm[E::pad(t + NT * i)];
-  __syncthreads();       // tile reads done before the transform reuses sm
-  E::run(v, sm, t, tr, xs);
-  const int col = col0 + team;
-  if constexpr (MODE != COL_INV_OUT) {
-    // twiddle W_P^{n2 k1}, k1 = t + NT*i
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint64_t k1 = uint64_t(t + NT * i);
-      v[i] = cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (k1 * uint64_t(col)) & Pmask, p.lfBig));
-      if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+    __syncthreads();
+    C v[R];
+  #pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = sm[E::pad(t + NT * i)];
+    __syncthreads();       // tile reads done before the transform reuses sm
+    E::run(v, sm, t, tr, xs);
+    const int col = col0 + team;
+    if constexpr (MODE != COL_INV_OUT) {
+      // twiddle W_P^{n2 k1}, k1 = t + NT*i
+  #pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint64_t k1 = uint64_t(t + NT * i);
+        v[i] = cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (k1 * uint64_t(col)) & Pmask, p.lfBig));
+        if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+      }
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
-  __syncthreads();
-  {
-    const int tau = threadIdx.x & (kColTile - 1);
-    for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
-      const C val = smbase[tau * CS + E::pad(row)];
-      if constexpr (MODE != COL_INV_OUT) {
-        reinterpret_cast<C*>(p.A)[int64_t(row) * P2 + col0 + tau] = val;
-      } else {
-        const int64_t mm = int64_t(col0 + tau) + P2 * row;  // m = c + P2 d
-        if (mm < p.m)
-          reinterpret_cast<C*>(p.X)[mm] = cmul(cconj(val), __ldg(reinterpret_cast<const C*>(p.chirp) + mm));
+    __syncthreads();
+  #pragma unroll
+    for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
+    __syncthreads();
+    {
+      const int tau = threadIdx.x & (kColTile - 1);
+      for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
+        const C val = smbase[tau * CS + E::pad(row)];
+        if constexpr (MODE != COL_INV_OUT) {
+          reinterpret_cast<C*>(p.A)[int64_t(row) * P2 + col0 + tau] = val;
+        } else {
+          const int64_t mm = int64_t(col0 + tau) + P2 * row;  // m = c + P2 d
+          if (mm < p.m)
+            reinterpret_cast<C*>(p.X)[mm] = cmul(cconj(val), __ldg(reinterpret_cast<const C*>(p.chirp) + mm));
+        }
       }
     }
   }
