@@ -139,7 +139,9 @@ int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype
  * block, dynamic shared memory; *staged bit 0 = rows TMA-staged, bits 1.. =
  * kernel variant (0 plain, 1 chirp tables in tensor memory, 2 the P = 16384
  * complex64 group-local chirp kernel k_chirp_local, 3 the α-FFT with two
- * teams per CTA splitting one signal's residues). */
+ * teams per CTA splitting one signal's residues, 4 the complex128 N = 4096
+ * α = 1/2 group-local α-FFT k_afft_local, 6 the P = 8192 complex128
+ * group-local chirp kernel k_chirp_local128). */
 int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged);
 
 const char* asx_strerror(int status);
