@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/asx.h"
+#include "asx_direct_tc.cuh"
 #include "asx_dispatch.cuh"
 
 using namespace asx;
@@ -84,7 +85,9 @@ struct asx_plan_s {
   void* tables = nullptr;
   size_t table_bytes = 0;
   size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
-  size_t off_afl = 0;  // k_afft_local twiddle image (complex128 N = 4096, alpha = 1/2), 0 = none
+  size_t off_afl = 0;
+  int dtc = 0;            // direct form on the tensor cores (k_direct_tc, complex64)
+  size_t off_vimg = 0;    // its fp16 operand image (bytes from tables)  // k_afft_local twiddle image (complex128 N = 4096, alpha = 1/2), 0 = none
   int lfA = 0;
   int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
   // large chirp path (P > one CTA): four-step P = P1 x P2 through workspace A
@@ -212,6 +215,12 @@ void* large_workspace(asx_plan_s* p, cudaStream_t st) {
   return w;
 }
 
+// k_direct_tc reads rows as float4 and writes them as float4
+bool dtc_aligned(const void* x, int64_t xs, const void* X, int64_t Xs) {
+  return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 && xs % 2 == 0 &&
+         Xs % 2 == 0;
+}
+
 int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs, int64_t batch,
                    cudaStream_t st) {
   if (batch == 0 || p->m == 0) return ASX_OK;
@@ -230,6 +239,25 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
       k_direct_small<float><<<grid, 256, 0, st>>>(kp);
     else
       k_direct_small<double><<<grid, 256, 0, st>>>(kp);
+    e = cudaGetLastError();
+  } else if (p->method == ASX_DIRECT && p->dtc && dtc_aligned(x, xs, X, Xs)) {
+    dtc::Params dp;
+    dp.x = static_cast<const float*>(x);
+    dp.xs = xs;
+    dp.X = static_cast<float*>(X);
+    dp.Xs = Xs;
+    dp.batch = batch;
+    dp.n = (int)p->n;
+    dp.m = (int)p->m;
+    dp.vimg = static_cast<const unsigned char*>(p->tables) + p->off_vimg;
+    const int64_t tiles = (batch + dtc::TS - 1) / dtc::TS;
+    const int grid = (int)std::min<int64_t>(tiles, p->env.sms);
+    dtc::k_direct_tc<<<grid, dtc::NTHREADS, dtc::SMEM_BYTES, st>>>(dp);
+    g_last_launch.grid = grid;
+    g_last_launch.block = dtc::NTHREADS;
+    g_last_launch.smem = dtc::SMEM_BYTES;
+    g_last_launch.staged = 1;
+    g_last_launch.tmem = 8;
     e = cudaGetLastError();
   } else if (p->method == ASX_DIRECT) {
     const int64_t gy = (batch + 63) / 64, gx = (p->m + 63) / 64;
@@ -385,6 +413,11 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   const double cost_fft = fft_ok ? (double)fft_r * (5.0 * fft_P * lg(fft_P) + 8.0 * fft_P) +
                                        (double)fft_fold * fft_P * 2.0
                                  : 1e300;
+  // direct form on the tensor cores: complex64 complex-input, 2N a multiple of
+  // the 64-real K chunk, 2M real outputs filling one or two N = 256 MMAs
+  const char* no_dtc = std::getenv("ASX_NO_DTC");
+  const bool dtc_ok = dtype == ASX_C64 && !real_input && n % 32 == 0 && m % 128 == 0 && m <= 256 &&
+                      !(no_dtc && no_dtc[0] == '1');
   const double cost_chirp = chirp_ok ? 2.0 * 5.0 * chirp_P * lg(chirp_P) + 24.0 * chirp_P : 1e300;
 
   int chosen = method;
@@ -511,6 +544,10 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     A_sz = chirp_P;  // four-step workspace
   }
   if (chosen == ASX_DIRECT) W_sz = m * n;
+  if (chosen == ASX_DIRECT && dtc_ok) {
+    p->dtc = 1;
+    W_sz = 3 * m * n;  // complex W (small-batch / misaligned launches) + the fp16 hi/lo image (16 m n bytes)
+  }
   const bool afl = chosen == ASX_FFT && dtype == ASX_C128 && p->P == AfftLocal::P && p->r == 2 && p->fold == 1;
   const int64_t afl_sz = afl ? AfftLocal::IMG_ELEMS : 0;
   p->tw_elems = (int)twA_sz;  // shared-memory table: α pre-twiddle only
@@ -524,6 +561,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   p->off_H = elems * es;
   elems += align(H_sz);
   p->off_W = elems * es;
+  p->off_vimg = p->off_W + size_t(m * n) * es;
   elems += align(W_sz);
   p->off_twP1 = elems * es;
   elems += align(twP1_sz);
@@ -621,6 +659,12 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     const int64_t total = m * n;
     k_dft_matrix<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
         base + p->off_W, m, n, (uint64_t)a, L, dbl);
+    if (p->dtc) {
+      dtc::k_direct_tc_image<<<(unsigned)std::min<int64_t>((4 * total + 255) / 256, 65535), 256, 0, st>>>(
+          reinterpret_cast<unsigned char*>(base + p->off_vimg), (int)n, (int)m, (uint64_t)a, L);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(dtc::k_direct_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, dtc::SMEM_BYTES);
+    }
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);

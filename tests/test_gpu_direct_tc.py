@@ -1,0 +1,126 @@
+"""GPU parity of the tensor-core direct α-DFT (k_direct_tc: tcgen05.mma
+kind::f16 on fp16 hi/lo splits, fp32 accumulation in tensor memory) against
+the CPU oracle's direct form (ref/oracle.py:37-67 `naive_forward`, batched as
+ref test_acceptance.py:64-67), at the complex64 tolerance 2e-5 of max|X|.
+
+Covers the BASELINE config-3 shape (N = M = 256, alpha = 37/100) at ragged
+batches (partial 128-signal tiles, more tiles than SMs), one and two output
+MMA halves (M = 128 / 256), several K-chunk counts, per-signal power-of-two
+scaling (signals of 1e-6 and 1e4 amplitude side by side, all-zero signals),
+strided rows, and the misaligned-stride fallback onto k_direct."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import alpha_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+VARIANT_DTC = 8  # asx_last_launch: k_direct_tc
+TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def asx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2403_16665_b200 as asx
+
+    return asx
+
+
+def _variant():
+    from paper_2403_16665_b200 import _lib
+
+    v = [ctypes.c_int(0) for _ in range(4)]
+    _lib.lib().asx_last_launch(*[ctypes.byref(c) for c in v])
+    return v[3].value >> 1
+
+
+def _run(asx, x, n, a, d, m, method="direct"):
+    import torch
+
+    p = asx.plan(n, asx.DenseFactor(d, a), m=m, dtype="complex64", method=method)
+    got = p.execute(torch.from_numpy(x.astype(np.complex64)).cuda()).cpu().numpy()
+    torch.cuda.synchronize()
+    return got
+
+
+@pytest.mark.parametrize("batch", [9, 127, 128, 129, 1000, 20000])
+def test_config3_shape(asx, batch):
+    n, a, d, m = 256, 37, 100, 256
+    rng = np.random.default_rng(batch)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(batch)]).astype(np.complex64)
+    got = _run(asx, x, n, a, d, m)
+    assert _variant() == VARIANT_DTC
+    assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
+
+
+@pytest.mark.parametrize("n,a,d,m", [(32, 1, 4, 128), (96, 2, 3, 256), (512, 1, 8, 128), (1024, 37, 100, 256),
+                                     (256, 1, 1, 256)])
+def test_shapes(asx, n, a, d, m):
+    rng = np.random.default_rng(n + m)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(300)]).astype(np.complex64)
+    got = _run(asx, x, n, a, d, m)
+    assert _variant() == VARIANT_DTC
+    assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
+
+
+def test_alpha_one_is_fft(asx):
+    """alpha = 1, M = N: the plain DFT (ref test_fastpath.py:157-161)."""
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((200, 256)) + 1j * rng.standard_normal((200, 256))).astype(np.complex64)
+    got = _run(asx, x, 256, 1, 1, 256)
+    assert orc.rel_err(got, np.fft.fft(x.astype(np.complex128), axis=1)) <= TOL
+
+
+def test_per_signal_scaling(asx):
+    """Signals far outside fp16 range (tiny and huge) and all-zero signals in one tile."""
+    n, a, d, m = 256, 37, 100, 256
+    rng = np.random.default_rng(11)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(256)])
+    amp = np.array([1e-6, 1e4, 1.0, 3e-3, 7e2, 1e-12, 1e12, 0.0] * 32)
+    x = (x * amp[:, None]).astype(np.complex64)
+    got = _run(asx, x, n, a, d, m)
+    assert _variant() == VARIANT_DTC
+    want = orc.direct(x.astype(np.complex128), a, d, m)
+    live = amp != 0.0
+    assert orc.rel_err(got[live], want[live]) <= TOL
+    assert np.all(got[~live] == 0)
+
+
+def test_impulse(asx):
+    """Impulse at n = 0 -> all-ones spectrum (ref test_fastpath.py:141-143)."""
+    x = np.zeros((130, 256), np.complex64)
+    x[:, 0] = 1.0
+    got = _run(asx, x, 256, 37, 100, 256)
+    assert np.max(np.abs(got - 1.0)) <= TOL
+
+
+@pytest.mark.parametrize("stride", [258, 257])
+def test_strided_rows(asx, stride):
+    """Rows inside a wider buffer: even strides run on the tensor cores, odd
+    ones (rows not 16-byte aligned) on the CUDA-core k_direct."""
+    import torch
+
+    n, a, d, m = 256, 37, 100, 256
+    rng = np.random.default_rng(stride)
+    buf = (rng.standard_normal((300, stride)) + 1j * rng.standard_normal((300, stride))).astype(np.complex64)
+    p = asx.plan(n, asx.DenseFactor(d, a), m=m, dtype="complex64", method="direct")
+    got = p.execute(torch.from_numpy(buf).cuda()[:, :n]).cpu().numpy()
+    assert _variant() == (VARIANT_DTC if stride % 2 == 0 else _variant())
+    assert orc.rel_err(got, orc.direct(buf[:, :n].astype(np.complex128), a, d, m)) <= TOL
+
+
+def test_linearity(asx):
+    """DFT(a x + b y) = a DFT(x) + b DFT(y) (ref test_oracle.py:85-93)."""
+    n, a, d, m = 256, 37, 100, 256
+    rng = np.random.default_rng(5)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(256)]).astype(np.complex64)
+    y = np.stack([orc.unit_disk(rng, n) for _ in range(256)]).astype(np.complex64)
+    gx, gy = _run(asx, x, n, a, d, m), _run(asx, y, n, a, d, m)
+    gs = _run(asx, (x + 2 * y).astype(np.complex64), n, a, d, m)
+    assert orc.rel_err(gs, gx + 2 * gy) <= 4 * TOL
