@@ -87,7 +87,8 @@ struct asx_plan_s {
   size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
   size_t off_afl = 0;
   int dtc = 0;            // direct form on the tensor cores (k_direct_tc, complex64)
-  size_t off_vimg = 0;    // its fp16 operand image (bytes from tables)  // k_afft_local twiddle image (complex128 N = 4096, alpha = 1/2), 0 = none
+  size_t off_vimg = 0;    // its fp16 operand image (bytes from tables)
+  int dtc_dbg = 0;        // env ASX_DTC_DBG: timing-only ablations of k_direct_tc  // k_afft_local twiddle image (complex128 N = 4096, alpha = 1/2), 0 = none
   int lfA = 0;
   int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
   // large chirp path (P > one CTA): four-step P = P1 x P2 through workspace A
@@ -249,7 +250,8 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
     dp.batch = batch;
     dp.n = (int)p->n;
     dp.m = (int)p->m;
-    dp.vimg = static_cast<const unsigned char*>(p->tables) + p->off_vimg;
+    dp.wimg = static_cast<const unsigned char*>(p->tables) + p->off_vimg;
+    dp.dbg = p->dtc_dbg;
     const int64_t tiles = (batch + dtc::TS - 1) / dtc::TS;
     const int grid = (int)std::min<int64_t>(tiles, p->env.sms);
     dtc::k_direct_tc<<<grid, dtc::NTHREADS, dtc::SMEM_BYTES, st>>>(dp);
@@ -416,7 +418,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   // direct form on the tensor cores: complex64 complex-input, 2N a multiple of
   // the 64-real K chunk, 2M real outputs filling one or two N = 256 MMAs
   const char* no_dtc = std::getenv("ASX_NO_DTC");
-  const bool dtc_ok = dtype == ASX_C64 && !real_input && n % 32 == 0 && m % 128 == 0 && m <= 256 &&
+  const bool dtc_ok = dtype == ASX_C64 && !real_input && n % 32 == 0 && (m == 128 || m == 256) &&
                       !(no_dtc && no_dtc[0] == '1');
   const double cost_chirp = chirp_ok ? 2.0 * 5.0 * chirp_P * lg(chirp_P) + 24.0 * chirp_P : 1e300;
 
@@ -546,7 +548,9 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   if (chosen == ASX_DIRECT) W_sz = m * n;
   if (chosen == ASX_DIRECT && dtc_ok) {
     p->dtc = 1;
-    W_sz = 3 * m * n;  // complex W (small-batch / misaligned launches) + the fp16 hi/lo image (16 m n bytes)
+    const char* dbg = std::getenv("ASX_DTC_DBG");
+    p->dtc_dbg = dbg ? std::atoi(dbg) : 0;
+    W_sz = 2 * m * n;  // complex W (small-batch / misaligned launches) + the fp16 Wr/Wi hi/lo image (8 m n bytes)
   }
   const bool afl = chosen == ASX_FFT && dtype == ASX_C128 && p->P == AfftLocal::P && p->r == 2 && p->fold == 1;
   const int64_t afl_sz = afl ? AfftLocal::IMG_ELEMS : 0;
@@ -660,7 +664,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     k_dft_matrix<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
         base + p->off_W, m, n, (uint64_t)a, L, dbl);
     if (p->dtc) {
-      dtc::k_direct_tc_image<<<(unsigned)std::min<int64_t>((4 * total + 255) / 256, 65535), 256, 0, st>>>(
+      dtc::k_direct_tc_image<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
           reinterpret_cast<unsigned char*>(base + p->off_vimg), (int)n, (int)m, (uint64_t)a, L);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(dtc::k_direct_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, dtc::SMEM_BYTES);

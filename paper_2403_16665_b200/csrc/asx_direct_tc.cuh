@@ -3,32 +3,31 @@
 //
 // The direct form (oracle.py:37-67 `_reduced_product` / `naive_forward`,
 // batched as the reference's acceptance test does, test_acceptance.py:64-67)
-// is the contraction X[b, m] = Σ_n x[b, n]·W[m, n].  Read as reals it is one
-// GEMM with no reshuffling of the data:
+// is the contraction X[b, m] = Σ_n x[b, n]·W[m, n].  In real arithmetic
 //
-//     C[b, j] = Σ_k A[b, k] · V[j, k]       A = x as float[B][2N] (re, im interleaved)
-//                                             C = X as float[B][2M]
-//     V[2m,   2n] =  Re W   V[2m,   2n+1] = -Im W
-//     V[2m+1, 2n] =  Im W   V[2m+1, 2n+1] =  Re W
+//     Re X = Ar·Wrᵀ − Ai·Wiᵀ        Im X = Ar·Wiᵀ + Ai·Wrᵀ
 //
-// complex64 needs ~fp32 products (tolerance 2e-5 of max|X|).  Each operand is
-// split into two fp16 terms, v = hi + lo, hi = fp16(v), lo = fp16(v - hi),
-// and C = A_hi·V_hi + A_hi·V_lo + A_lo·V_hi with fp32 accumulation (the
-// dropped lo·lo term is ~2^-22 relative).  To keep the fp16 terms in range for
-// any input, every signal is scaled by a power of two so that its max |x|
-// lands in [2^10, 2^11), V by 2^8; the epilogue multiplies the exact inverse.
+// four real GEMMs over the de-interleaved signal (Ar, Ai) and the plan's
+// W = Wr + i·Wi; the minus is the MMA's A-negate bit.  complex64 needs ~fp32
+// products (tolerance 2e-5 of max|X|): each operand is split into two fp16
+// terms, v = hi + lo (hi = fp16(v), lo = fp16(v − hi)), and every real GEMM is
+// A_hi·B_hi + A_hi·B_lo + A_lo·B_hi with fp32 accumulation (the dropped lo·lo
+// term is ~2^-22 relative).  To keep the fp16 terms in range for any input,
+// each signal is scaled by a power of two so its max |x| lands in
+// [2^10, 2^11), W by 2^8; the epilogue multiplies the exact inverse.
 //
 // One persistent CTA per SM, 128 signals per tile (= MMA M = the 128 TMEM
-// lanes), all 2M <= 512 output reals of the tile accumulated in TMEM (N = 256
-// per MMA, M <= 256 bins).  K streams in chunks of 64 reals (one 128-byte
-// swizzled fp16 row per operand row):
-//   warps 0-7   convert: x (fp32, coalesced float4 loads) -> scaled fp16 hi/lo
-//               in the SWIZZLE_128B K-major layout, 2-stage ring; then the
-//               epilogue of the previous tile (tcgen05.ld -> scale -> store)
-//   warp 8      one elected thread issues the MMAs (3 per 16-wide K step)
-//   warp 9      one thread streams V's plan-time fp16 image (already swizzled)
-//               by 1-D TMA bulk copies, 2-stage ring of 64 KB stages
-//   warps 10-13 per-signal scales of the next tile (first, HBM-bound read of x)
+// lanes); Re X and Im X of the tile (M <= 256 bins each) accumulate in TMEM
+// columns [0, M) and [M, 2M).  K streams in chunks of 32 samples, operands in
+// the K-major SWIZZLE_64B layout (64-byte fp16 rows):
+//   warps 0-7   convert: x (fp32, coalesced loads) -> scaled, de-interleaved
+//               fp16 hi/lo (Ar, Ai), 2-stage ring; then the epilogue of the
+//               previous tile (tcgen05.ld -> scale -> interleaved stores)
+//   warp 8      one elected thread issues the MMAs (12 per 32-sample part)
+//   warp 9      one thread streams W's plan-time fp16 image (already swizzled)
+//               by 1-D TMA bulk copies, 4-stage ring (Wr / Wi parts of a chunk)
+//   warps 10-13 per-signal scales of the next tile (the first, HBM-bound read
+//               of x; it leaves the tile in L2 for the converters)
 // ---------------------------------------------------------------------------
 #pragma once
 
@@ -39,19 +38,21 @@
 namespace asx {
 namespace dtc {
 
-constexpr int TS = 128;                   // signals per tile
-constexpr int KC = 64;                    // reals per K chunk
-constexpr int NMMA = 256;                 // output reals per MMA
-constexpr int NCONV = 256;                // converter / epilogue threads
-constexpr int NSCALE = 128;               // row-scale warps (one tile ahead; their reads warm L2)
-constexpr int NTHREADS = NCONV + 64 + NSCALE;  // + MMA warp + V-loader warp + scale warps
-constexpr int A_HALF = TS * KC * 2;       // one fp16 term of an A stage: 16 KB
-constexpr int A_STAGE = 2 * A_HALF;       // hi + lo
-constexpr int B_HALF = NMMA * KC * 2;     // 32 KB
-constexpr int B_STAGE = 2 * B_HALF;       // hi + lo: 64 KB
-constexpr int NA = 2, NB = 2;
-constexpr float V_SCALE = 256.0f;
-constexpr int SMEM_BYTES = 1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 1024 /*bars, slot*/ + 2 * TS * 4 /*scales*/;
+constexpr int TS = 128;                    // signals per tile
+constexpr int KC = 32;                     // samples per K chunk (64-byte fp16 rows)
+constexpr int NCONV = 256;                 // converter / epilogue threads
+constexpr int NSCALE = 256;                // row-scale threads
+constexpr int NTHREADS = NCONV + 64 + NSCALE;
+constexpr int A_TERM = TS * KC * 2;        // one fp16 term of Ar or Ai: 8 KB
+constexpr int A_STAGE = 4 * A_TERM;        // [Ar hi | Ar lo | Ai hi | Ai lo]
+constexpr int MMAX = 256;                  // bins per tile (MMA N)
+constexpr int B_STAGE = 2 * MMAX * KC * 2; // one part (Wr or Wi) [hi | lo] at M = 256: 32 KB
+constexpr int NA = 2, NB = 3;
+constexpr int EPI_LD = 36;                 // staging row stride (floats): 16 bins + pad, conflict-free
+constexpr int EPI_WARP = 32 * EPI_LD * 4;  // per-warp output staging: 4.5 KB
+constexpr float W_SCALE = 256.0f;
+constexpr int SMEM_BYTES =
+    1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 512 /*bars, slot*/ + 2 * TS * 4 /*scales*/ + 8 * EPI_WARP;
 constexpr int TMEM_COLS = 512;
 
 struct Params {
@@ -60,30 +61,36 @@ struct Params {
   float* X;
   int64_t Xs;       // output row stride, complex elements
   int64_t batch;
-  int n, m;         // complex length / bins; 2n % 64 == 0, m % 128 == 0, m <= 256
-  const unsigned char* vimg;  // plan-time image: [kc][half][hi|lo][256][64] fp16, swizzled
+  int n, m;         // n % 32 == 0; m in {128, 256}
+  const unsigned char* wimg;  // plan-time image: [chunk][Wr | Wi][hi | lo][m][32] fp16, swizzled
+  int dbg;          // timing-only ablations (env ASX_DTC_DBG, wrong results): 1 no MMAs, 2 no epilogue
+                    // drain, 4 no x loads in the converters
 };
 
-// byte offset of element (row, k) of a K-major SWIZZLE_128B tile of 64-wide fp16 rows
+// byte offset of element (row, k) in a K-major SWIZZLE_64B tile of 32-wide fp16
+// rows: the 16-byte unit index (address bits 4-5) XOR address bits 7-8
 __host__ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t k) {
-  return row * 128u + ((((k >> 3) ^ (row & 7u)) & 7u) << 4) + (k & 7u) * 2u;
+  const uint32_t off = row * 64u + k * 2u;
+  return off ^ (((off >> 7) & 3u) << 4);
 }
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4)  // start address
          | ((uint64_t)1 << 16)                 // LBO (unused for swizzled K-major)
-         | ((uint64_t)(1024 >> 4) << 32)       // SBO: 8 rows x 128 B
+         | ((uint64_t)(512 >> 4) << 32)        // SBO: 8 rows x 64 B
          | ((uint64_t)1 << 46)                 // sm_100 descriptor version
-         | ((uint64_t)2 << 61);                // SWIZZLE_128B
+         | ((uint64_t)4 << 61);                // SWIZZLE_64B
 }
-// kind::f16: fp16 x fp16 -> fp32, both K-major, M = 128, N = 256
-constexpr uint32_t IDESC = (1u << 4) | (uint32_t(NMMA >> 3) << 17) | (uint32_t(TS >> 4) << 24);
+// kind::f16: fp16 x fp16 -> fp32, both K-major, M = 128, N = m
+__device__ __forceinline__ uint32_t idesc(int n, bool neg_a) {
+  return (1u << 4) | (neg_a ? (1u << 13) : 0u) | (uint32_t(n >> 3) << 17) | (uint32_t(TS >> 4) << 24);
+}
 
-__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
+      "l"(a), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -93,8 +100,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-      "tcgen05.wait::ld.sync.aligned;"
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
         "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
@@ -102,42 +108,48 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr)
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
-__device__ __forceinline__ void split4(float4 v, float s, uint2& hi, uint2& lo) {
-  const float f[4] = {v.x * s, v.y * s, v.z * s, v.w * s};
-  __half h[4], l[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    h[i] = __float2half_rn(f[i]);
-    l[i] = __float2half_rn(f[i] - __half2float(h[i]));
-  }
-  hi = make_uint2(pack_h2(h[0], h[1]), pack_h2(h[2], h[3]));
-  lo = make_uint2(pack_h2(l[0], l[1]), pack_h2(l[2], l[3]));
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+  hi = pack_h2(ha, hb);
+  lo = pack_h2(__float2half_rn(a - __half2float(ha)), __float2half_rn(b - __half2float(hb)));
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = smem;                       // NA x [hi 16 KB | lo 16 KB]
-  unsigned char* sB = smem + NA * A_STAGE;        // NB x [hi 32 KB | lo 32 KB]
+  unsigned char* sA = smem;                 // NA x A_STAGE
+  unsigned char* sB = smem + NA * A_STAGE;  // NB x B_STAGE
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NB * B_STAGE);
-  uint64_t* a_full = bars;           // NA, count NCONV
-  uint64_t* a_empty = bars + NA;     // NA, tcgen05.commit
-  uint64_t* b_full = bars + 2 * NA;  // NB, TMA tx
-  uint64_t* b_empty = b_full + NB;   // NB, tcgen05.commit
-  uint64_t* acc_full = b_empty + NB; // tcgen05.commit
+  uint64_t* a_full = bars;             // NA, count NCONV
+  uint64_t* a_empty = a_full + NA;     // NA, tcgen05.commit
+  uint64_t* b_full = a_empty + NA;     // NB, TMA tx
+  uint64_t* b_empty = b_full + NB;     // NB, tcgen05.commit
+  uint64_t* acc_full = b_empty + NB;   // tcgen05.commit
   uint64_t* acc_empty = acc_full + 1;  // count NCONV
   uint64_t* sc_full = acc_empty + 1;   // 2, count NSCALE
   uint64_t* sc_empty = sc_full + 2;    // 2, count NCONV
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_empty + 2);
-  float* scale = reinterpret_cast<float*>(smem + NA * A_STAGE + NB * B_STAGE + 1024);  // [2][TS]
+  float* scale = reinterpret_cast<float*>(sB + NB * B_STAGE + 512);  // [2][TS]
+  float* epi_stage = scale + 2 * TS;                                   // 8 x [32][EPI_LD]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kcn = (2 * p.n) / KC;       // K chunks
-  const int nh = (2 * p.m) / NMMA;      // MMAs per K step (output halves)
+  const int kcn = p.n / KC;                 // K chunks
+  const int m = p.m;
+  const int b_bytes = 2 * m * KC * 2;       // one part [hi | lo]
   const int64_t ntiles = (p.batch + TS - 1) / TS;
 
   if (tid == 0) {
@@ -168,52 +180,76 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     uint32_t ca = 0;  // A chunks produced
     int64_t prev = -1;
     uint32_t ntile_done = 0;
+    // chunk c of tile t: 128 rows x 32 complex = 128 rows x 256 bytes of x;
+    // a thread takes 4 consecutive complex (two float4) of a row, 4 times
     auto convert = [&](int64_t t, int buf, int c) {
       const uint32_t s = ca % NA;
-      float4 v[8];
+      float4 v[4][2];
       const float* sc = scale + buf * TS;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int q = tid + NCONV * i, row = q >> 4, c4 = q & 15;
+      for (int i = 0; i < 4; ++i) {
+        const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
         const int64_t b = t * TS + row;
-        v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b < p.batch)
-          v[i] = __ldg(reinterpret_cast<const float4*>(p.x + b * 2 * p.xs + c * KC + c4 * 4));
+        v[i][0] = v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < p.batch && !(p.dbg & 4)) {
+          const float4* src = reinterpret_cast<const float4*>(p.x + b * 2 * p.xs + (int64_t)c * 2 * KC) + 2 * g;
+          v[i][0] = __ldcs(src);
+          v[i][1] = __ldcs(src + 1);
+        }
       }
       mbar_wait(&a_empty[s], ((ca / NA) & 1) ^ 1);
       unsigned char* st = sA + s * A_STAGE;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int q = tid + NCONV * i, row = q >> 4, c4 = q & 15;
-        uint2 hi, lo;
-        split4(v[i], sc[row], hi, lo);
-        const uint32_t off = swz(row, c4 * 4);
-        *reinterpret_cast<uint2*>(st + off) = hi;
-        *reinterpret_cast<uint2*>(st + A_HALF + off) = lo;
+      for (int i = 0; i < 4; ++i) {
+        const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
+        const float f = sc[row];
+        uint2 rh, rl, ih, il;
+        split2(v[i][0].x * f, v[i][0].z * f, rh.x, rl.x);
+        split2(v[i][1].x * f, v[i][1].z * f, rh.y, rl.y);
+        split2(v[i][0].y * f, v[i][0].w * f, ih.x, il.x);
+        split2(v[i][1].y * f, v[i][1].w * f, ih.y, il.y);
+        const uint32_t off = swz(row, 4 * g);
+        *reinterpret_cast<uint2*>(st + off) = rh;
+        *reinterpret_cast<uint2*>(st + A_TERM + off) = rl;
+        *reinterpret_cast<uint2*>(st + 2 * A_TERM + off) = ih;
+        *reinterpret_cast<uint2*>(st + 3 * A_TERM + off) = il;
       }
       fence_proxy_async();
       mbar_arrive(&a_full[s]);
       ++ca;
     };
+    // Re in TMEM columns [0, m), Im in [m, 2m); warp (q, h) drains lanes
+    // 32q..32q+31 (its signals) and bins [h m/2, (h+1) m/2)
     auto epilogue = [&](int64_t t, int buf) {
       mbar_wait(acc_full, ntile_done & 1);
       tmem_fence_after();
       const int q = warp & 3, h = warp >> 2;
       const int r = q * 32 + lane;
-      const int64_t b = t * TS + r;
-      const float inv = 1.f / (scale[buf * TS + r] * V_SCALE);
-      const int cols = p.m;  // output reals per warp group (2m split in two)
-      for (int c0 = 0; c0 < cols; c0 += 32) {
-        uint32_t w[32];
-        const int col = h * cols + c0;
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)col, w);
-        if (b < p.batch) {
-          float4* dst = reinterpret_cast<float4*>(p.X + b * 2 * p.Xs + col);
+      const float inv = 1.f / (scale[buf * TS + r] * W_SCALE);
+      const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+      // 16 bins per round: each thread stages its signal's 16 complex outputs,
+      // then the warp writes 4 signals' 128-byte row segments per store
+      float* stg = epi_stage + warp * (32 * EPI_LD);
+      const int64_t b0 = t * TS + q * 32;
+      for (int c0 = h * (m / 2); c0 < (h + 1) * (m / 2) && !(p.dbg & 2); c0 += 16) {
+        uint32_t re[16], im[16];
+        tmem_ld16(lane_base + (uint32_t)c0, re);
+        tmem_ld16(lane_base + (uint32_t)(m + c0), im);
+        tmem_wait_ld();
+        float4* srow = reinterpret_cast<float4*>(stg + lane * EPI_LD);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(w[4 * i]) * inv, __uint_as_float(w[4 * i + 1]) * inv,
-                                 __uint_as_float(w[4 * i + 2]) * inv, __uint_as_float(w[4 * i + 3]) * inv);
+        for (int i = 0; i < 8; ++i)
+          srow[i] = make_float4(__uint_as_float(re[2 * i]) * inv, __uint_as_float(im[2 * i]) * inv,
+                                __uint_as_float(re[2 * i + 1]) * inv, __uint_as_float(im[2 * i + 1]) * inv);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = 4 * i + (lane >> 3), j = lane & 7;
+          const int64_t bb = b0 + rr;
+          const float4 v = reinterpret_cast<const float4*>(stg + rr * EPI_LD)[j];
+          if (bb < p.batch) __stcs(reinterpret_cast<float4*>(p.X + bb * 2 * p.Xs + 2 * c0) + j, v);
         }
+        __syncwarp();
       }
       tmem_fence_before();
       mbar_arrive(acc_empty);
@@ -237,6 +273,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     if (lane == 0) {
       uint32_t ca = 0, cb = 0, nt = 0;
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      const uint32_t id = idesc(m, false), idn = idesc(m, true);
+      const uint32_t d_re = tmem, d_im = tmem + (uint32_t)m;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         if (nt > 0) {
           mbar_wait(acc_empty, (nt - 1) & 1);
@@ -246,19 +284,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
           const uint32_t sa = ca % NA;
           mbar_wait(&a_full[sa], (ca / NA) & 1);
           tmem_fence_after();
-          const uint32_t ah = a0 + sa * A_STAGE, al = ah + A_HALF;
-          for (int hh = 0; hh < nh; ++hh) {
+          const uint32_t arh = a0 + sa * A_STAGE, arl = arh + A_TERM, aih = arl + A_TERM, ail = aih + A_TERM;
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {  // 0: Wr, 1: Wi
             const uint32_t sb = cb % NB;
             mbar_wait(&b_full[sb], (cb / NB) & 1);
             tmem_fence_after();
-            const uint32_t bh = b0 + sb * B_STAGE, bl = bh + B_HALF;
-            const uint32_t d = tmem + (uint32_t)(hh * NMMA);
+            const uint32_t bh = b0 + sb * B_STAGE, bl = bh + (uint32_t)(b_bytes / 2);
 #pragma unroll
             for (int k = 0; k < KC / 16; ++k) {
               const uint32_t ko = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
-              mma_f16(d, sdesc(ah + ko), sdesc(bh + ko), (c > 0 || k > 0) ? 1u : 0u);
-              mma_f16(d, sdesc(ah + ko), sdesc(bl + ko), 1u);
-              mma_f16(d, sdesc(al + ko), sdesc(bh + ko), 1u);
+              const uint64_t Bh = sdesc(bh + ko), Bl = sdesc(bl + ko);
+              if (p.dbg & 1) {
+              } else if (part == 0) {  // Re += Ar Wr,  Im += Ai Wr
+                const uint32_t first = (c == 0 && k == 0) ? 0u : 1u;
+                mma_f16(d_re, sdesc(arh + ko), Bh, id, first);
+                mma_f16(d_re, sdesc(arh + ko), Bl, id, 1u);
+                mma_f16(d_re, sdesc(arl + ko), Bh, id, 1u);
+                mma_f16(d_im, sdesc(aih + ko), Bh, id, first);
+                mma_f16(d_im, sdesc(aih + ko), Bl, id, 1u);
+                mma_f16(d_im, sdesc(ail + ko), Bh, id, 1u);
+              } else {  // Re -= Ai Wi,  Im += Ar Wi
+                mma_f16(d_re, sdesc(aih + ko), Bh, idn, 1u);
+                mma_f16(d_re, sdesc(aih + ko), Bl, idn, 1u);
+                mma_f16(d_re, sdesc(ail + ko), Bh, idn, 1u);
+                mma_f16(d_im, sdesc(arh + ko), Bh, id, 1u);
+                mma_f16(d_im, sdesc(arh + ko), Bl, id, 1u);
+                mma_f16(d_im, sdesc(arl + ko), Bh, id, 1u);
+              }
             }
             mma_commit(&b_empty[sb]);
             ++cb;
@@ -273,15 +326,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   } else if (warp >= 10) {
     // ---------------- row scales, one tile ahead of the converters ----------------
     // Power of two per signal so its max |x| lands in [2^10, 2^11).  Each warp
-    // takes 32 rows, four at a time with all their loads in flight; the reads
-    // also bring the tile into L2 for the converters.
+    // takes 32 rows, four at a time with all their loads in flight.
     const int sw = warp - 10;
+    // each thread pulls one row of the coming tile into L2 (bulk prefetch, no
+    // registers held) while the buffer it will fill is still in use
+    auto prefetch_tile = [&](int64_t t) {
+      const int r = tid - (NCONV + 64);
+      const int64_t b = t * TS + r;
+      if (r < TS && t < ntiles && b < p.batch)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.x + b * 2 * p.xs), "r"(8 * p.n)
+                     : "memory");
+    };
+    prefetch_tile(blockIdx.x);
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
       mbar_wait(&sc_empty[buf], ((it >> 1) & 1) ^ 1);
       float* sc = scale + buf * TS;
-      for (int r0 = sw * 32; r0 < sw * 32 + 32; r0 += 4) {
+      for (int r0 = sw * (TS / (NSCALE / 32)); r0 < (sw + 1) * (TS / (NSCALE / 32)); r0 += 4) {
         float mx[4] = {0.f, 0.f, 0.f, 0.f};
         const int nq = p.n / 2;  // float4 per row
         for (int i0 = 0; i0 < nq; i0 += 128) {
@@ -315,21 +377,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
         }
       }
       mbar_arrive(&sc_full[buf]);
+      prefetch_tile(t + gridDim.x);
     }
   } else {
-    // ------------------------------ V image loader ------------------------------
+    // ------------------------------ W image loader ------------------------------
     if (lane == 0) {
       uint32_t cb = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int c = 0; c < kcn; ++c) {
-          for (int hh = 0; hh < nh; ++hh) {
+          for (int part = 0; part < 2; ++part) {
             const uint32_t sb = cb % NB;
             mbar_wait(&b_empty[sb], ((cb / NB) & 1) ^ 1);
-            mbar_expect_tx(&b_full[sb], B_STAGE);
-            const unsigned char* src = p.vimg + (size_t)(c * nh + hh) * B_STAGE;
+            mbar_expect_tx(&b_full[sb], (uint32_t)b_bytes);
+            const unsigned char* src = p.wimg + (size_t)(2 * c + part) * b_bytes;
             unsigned char* dst = sB + sb * B_STAGE;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) tma_load_1d(dst + i * (B_STAGE / 4), src + i * (B_STAGE / 4), B_STAGE / 4, &b_full[sb]);
+            tma_load_1d(dst, src, (uint32_t)(b_bytes / 2), &b_full[sb]);
+            tma_load_1d(dst + b_bytes / 2, src + b_bytes / 2, (uint32_t)(b_bytes / 2), &b_full[sb]);
             ++cb;
           }
         }
@@ -343,32 +406,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   if (warp == 8) tmem_dealloc(tmem, TMEM_COLS);
 }
 
-// Plan time: the real-ified, scaled, fp16-split V image in the shared-memory
-// layout the MMA reads (so the loader is a plain bulk copy).  Phases use the
-// exact integer reduction (a·m·n) mod L of oracle.py:37-47 and sincospi.
+// Plan time: the scaled, fp16-split Wr / Wi image in the shared-memory layout
+// the MMA reads (so the loader is a plain bulk copy).  Phases use the exact
+// integer reduction (a·m·n) mod L of oracle.py:37-47 and sincospi.
 __global__ void k_direct_tc_image(unsigned char* img, int n, int m, uint64_t a, uint64_t L) {
-  const int nh = (2 * m) / NMMA;
-  const int64_t total = (int64_t)(2 * n) * (2 * m);
+  const int64_t total = (int64_t)n * m;
+  const size_t part_bytes = (size_t)2 * m * KC * 2, term_bytes = part_bytes / 2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(e / (2 * n)), kk = (int)(e % (2 * n));  // output real j, input real kk
-    const int mb = j >> 1, nn = kk >> 1;
+    const int mb = (int)(e / n), nn = (int)(e % n);
     const uint64_t ph = (uint64_t)(((unsigned __int128)((uint64_t)a * (uint64_t)mb) * (uint64_t)nn) % L);
     double sn, cs;
     sincospi(2.0 * (double)ph / (double)L, &sn, &cs);  // W = cs - i sn
-    const double wr = cs, wi = -sn;
-    double v;
-    if ((j & 1) == 0)
-      v = (kk & 1) == 0 ? wr : -wi;
-    else
-      v = (kk & 1) == 0 ? wi : wr;
-    v *= (double)V_SCALE;
-    const __half hi = __float2half_rn((float)v);
-    const __half lo = __float2half_rn((float)(v - (double)__half2float(hi)));
-    const int c = kk / KC, k = kk % KC, hh = j / NMMA, row = j % NMMA;
-    unsigned char* st = img + (size_t)(c * nh + hh) * B_STAGE;
-    const uint32_t off = swz((uint32_t)row, (uint32_t)k);
-    *reinterpret_cast<__half*>(st + off) = hi;
-    *reinterpret_cast<__half*>(st + B_HALF + off) = lo;
+    const double w[2] = {cs * (double)W_SCALE, -sn * (double)W_SCALE};
+    const int c = nn / KC, k = nn % KC;
+    const uint32_t off = swz((uint32_t)mb, (uint32_t)k);
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const __half hi = __float2half_rn((float)w[part]);
+      const __half lo = __float2half_rn((float)(w[part] - (double)__half2float(hi)));
+      unsigned char* st = img + (size_t)(2 * c + part) * part_bytes;
+      *reinterpret_cast<__half*>(st + off) = hi;
+      *reinterpret_cast<__half*>(st + term_bytes + off) = lo;
+    }
   }
 }
 
