@@ -66,6 +66,15 @@ def measured_peaks():
         return FALLBACK_HBM_GBS, "fallback"
 
 
+def tensor_peak():
+    """Dense fp16/bf16 tensor-core peak (TFLOP/s): MEASURED_PEAKS.json's cuBLAS bf16 burst figure."""
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["bf16_tflops"]), "measured bf16_tflops (MEASURED_PEAKS.json)"
+    except Exception:
+        return 2250.0, "nominal dense bf16/fp16"
+
+
 def fp_peak(dtype: str):
     """Measured FFMA / DFMA peak (TFLOP/s) of a pool B200 (scripts/fp_peaks.cu -> profiles/fp_peaks.json)."""
     try:
@@ -122,6 +131,8 @@ def launched_kernel(method: str) -> str:
         return "k_afft_local<double> (group-local alpha-FFT, csrc/asx_afft_local.cuh)"
     if method == "chirp" and variant == 6:
         return "k_chirp_local128<double> (group-local chirp-z, csrc/asx_chirp_local128.cuh)"
+    if method == "direct" and variant == 8:
+        return "k_direct_tc (tcgen05.mma kind::f16, fp16 hi/lo split, TMEM accumulators, csrc/asx_direct_tc.cuh)"
     if method == "direct":
         return "k_direct"
     kind = "afft" if method == "fft" else "chirp"
@@ -273,6 +284,15 @@ def side_config(key, dev, stream, peak, reps=20):
            "method": p.method, "kernel": kern, "ms_per_step": ms, "value": w.batch * w.m / (ms / 1e3),
            "unit": "complex points/s", "hbm_gbs": gbs, "hbm_frac": gbs / peak, "reps": reps,
            "traffic": profiled_traffic(key, p.method), "bytes_alg": w.bytes_alg(w.batch)}
+    if kern.startswith("k_direct_tc"):
+        # direct form: 8 M N flops per signal; the tensor cores execute 3x that
+        # (A_hi B_hi + A_hi B_lo + A_lo B_hi per real product)
+        flops = 8.0 * w.m * w.n * w.batch
+        tp, src = tensor_peak()
+        res["tensor"] = {"alg_tflops": flops / (ms / 1e3) / 1e12,
+                         "executed_tflops": 3 * flops / (ms / 1e3) / 1e12, "peak_tflops": tp,
+                         "frac": 3 * flops / (ms / 1e3) / 1e12 / tp, "peak_source": src,
+                         "flops": "8 M N per signal (direct form); executed = 3x (fp16 hi/lo split)"}
     del x, out
     torch.cuda.empty_cache()
     return res

@@ -411,15 +411,18 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   const bool chirp_ok = chirp_P <= maxP || chirp_large;
 
   auto lg = [](int64_t v) { return (double)std::max(1, log2i(v)); };
-  const double cost_direct = 8.0 * (double)n * (double)m * 0.5;
+  const double cost_direct_cuda = 8.0 * (double)n * (double)m * 0.5;
   const double cost_fft = fft_ok ? (double)fft_r * (5.0 * fft_P * lg(fft_P) + 8.0 * fft_P) +
                                        (double)fft_fold * fft_P * 2.0
                                  : 1e300;
-  // direct form on the tensor cores: complex64 complex-input, 2N a multiple of
-  // the 64-real K chunk, 2M real outputs filling one or two N = 256 MMAs
+  // direct form on the tensor cores (k_direct_tc): complex64 complex input,
+  // N a multiple of the 32-sample K chunk, M = 128 or 256 bins (Re and Im of
+  // the tile fill the 512 TMEM columns).  Cost in the same units, calibrated
+  // on config 3 (N = M = 256: 0.406 ms against the chirp path's 0.470 ms).
   const char* no_dtc = std::getenv("ASX_NO_DTC");
   const bool dtc_ok = dtype == ASX_C64 && !real_input && n % 32 == 0 && (m == 128 || m == 256) &&
                       !(no_dtc && no_dtc[0] == '1');
+  const double cost_direct = dtc_ok ? 0.75 * (double)n * (double)m : cost_direct_cuda;
   const double cost_chirp = chirp_ok ? 2.0 * 5.0 * chirp_P * lg(chirp_P) + 24.0 * chirp_P : 1e300;
 
   int chosen = method;
