@@ -141,7 +141,8 @@ int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype
  * complex64 group-local chirp kernel k_chirp_local, 3 the α-FFT with two
  * teams per CTA splitting one signal's residues, 4 the complex128 N = 4096
  * α = 1/2 group-local α-FFT k_afft_local, 6 the P = 8192 complex128
- * group-local chirp kernel k_chirp_local128). */
+ * group-local chirp kernel k_chirp_local128, 8 the tensor-core direct form
+ * k_direct_tc). */
 int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged);
 
 const char* asx_strerror(int status);
