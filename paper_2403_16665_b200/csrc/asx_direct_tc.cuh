@@ -26,7 +26,7 @@
 //   warp 8      one elected thread issues the MMAs (12 per 32-sample part)
 //   warp 9      one thread streams W's plan-time fp16 image (already swizzled)
 //               by 1-D TMA bulk copies, 4-stage ring (Wr / Wi parts of a chunk)
-//   warps 10-13 per-signal scales of the next tile (the first, HBM-bound read
+//   warps 10-17 per-signal scales of the next tile (the first, HBM-bound read
 //               of x; it leaves the tile in L2 for the converters)
 // ---------------------------------------------------------------------------
 #pragma once
@@ -328,16 +328,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     // Power of two per signal so its max |x| lands in [2^10, 2^11).  Each warp
     // takes 32 rows, four at a time with all their loads in flight.
     const int sw = warp - 10;
-    // each thread pulls one row of the coming tile into L2 (bulk prefetch, no
-    // registers held) while the buffer it will fill is still in use
-    auto prefetch_tile = [&](int64_t t) {
-      const int r = tid - (NCONV + 64);
-      const int64_t b = t * TS + r;
-      if (r < TS && t < ntiles && b < p.batch)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.x + b * 2 * p.xs), "r"(8 * p.n)
-                     : "memory");
-    };
-    prefetch_tile(blockIdx.x);
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
@@ -377,7 +367,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
         }
       }
       mbar_arrive(&sc_full[buf]);
-      prefetch_tile(t + gridDim.x);
     }
   } else {
     // ------------------------------ W image loader ------------------------------
