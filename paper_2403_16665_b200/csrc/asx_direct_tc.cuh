@@ -22,10 +22,11 @@
 // the K-major SWIZZLE_64B layout (64-byte fp16 rows):
 //   warps 0-7   convert: x (fp32, coalesced loads) -> scaled, de-interleaved
 //               fp16 hi/lo (Ar, Ai), 2-stage ring; then the epilogue of the
-//               previous tile (tcgen05.ld -> scale -> interleaved stores)
+//               previous tile (tcgen05.ld -> scale -> shared-memory transpose
+//               -> 128-byte row-segment streaming stores)
 //   warp 8      one elected thread issues the MMAs (12 per 32-sample part)
 //   warp 9      one thread streams W's plan-time fp16 image (already swizzled)
-//               by 1-D TMA bulk copies, 4-stage ring (Wr / Wi parts of a chunk)
+//               by 1-D TMA bulk copies, 3-stage ring (Wr / Wi parts of a chunk)
 //   warps 10-17 per-signal scales of the next tile (the first, HBM-bound read
 //               of x; it leaves the tile in L2 for the converters)
 // ---------------------------------------------------------------------------
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   } else if (warp >= 10) {
     // ---------------- row scales, one tile ahead of the converters ----------------
     // Power of two per signal so its max |x| lands in [2^10, 2^11).  Each warp
-    // takes 32 rows, four at a time with all their loads in flight.
+    // takes TS / 8 = 16 rows, four at a time with all their loads in flight.
     const int sw = warp - 10;
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
