@@ -22,8 +22,8 @@
 // the K-major SWIZZLE_64B layout (64-byte fp16 rows):
 //   warps 0-7   convert: x (fp32, coalesced loads) -> scaled, de-interleaved
 //               fp16 hi/lo (Ar, Ai), 2-stage ring; then the epilogue of the
-//               previous tile (tcgen05.ld -> scale -> shared-memory transpose
-//               -> 128-byte row-segment streaming stores)
+//               previous tile (tcgen05.ld 16x256b fragments -> scale ->
+//               streaming stores of 64-byte row segments, 8 signals each)
 //   warp 8      one elected thread issues the MMAs (12 per 32-sample part)
 //   warp 9      one thread streams W's plan-time fp16 image (already swizzled)
 //               by 1-D TMA bulk copies, 3-stage ring (Wr / Wi parts of a chunk)
@@ -35,6 +35,10 @@
 #include <cuda_fp16.h>
 
 #include "asx_engine.cuh"
+
+#ifndef ASX_DTC_EPI_FRAG
+#define ASX_DTC_EPI_FRAG 1  // epilogue: 16x256b TMEM fragments straight to global (0: 32x32b + smem transpose)
+#endif
 
 namespace asx {
 namespace dtc {
@@ -53,7 +57,8 @@ constexpr int EPI_LD = 36;                 // staging row stride (floats): 16 bi
 constexpr int EPI_WARP = 32 * EPI_LD * 4;  // per-warp output staging: 4.5 KB
 constexpr float W_SCALE = 256.0f;
 constexpr int SMEM_BYTES =
-    1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 512 /*bars, slot*/ + 2 * TS * 4 /*scales*/ + 8 * EPI_WARP;
+    1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 512 /*bars, slot*/ + 2 * TS * 4 /*scales*/ +
+    (ASX_DTC_EPI_FRAG ? 0 : 8 * EPI_WARP);
 constexpr int TMEM_COLS = 512;
 
 struct Params {
@@ -119,6 +124,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 16 lanes x 256 bit, 4 repetitions along the columns: r[4j + {0,1}] = lane
+// t/4, columns 8j + 2(t%4) + {0,1}; r[4j + {2,3}] = lane t/4 + 8, same columns
+__device__ __forceinline__ void tmem_ld16x256(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+// wait that also "writes" the loaded registers, so no use of them can be
+// scheduled above it (the loads complete asynchronously)
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&a)[16], uint32_t (&b)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+                 "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]),
+                 "+r"(a[15]), "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]),
+                 "+r"(b[7]), "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]), "+r"(b[13]),
+                 "+r"(b[14]), "+r"(b[15])
+               :
+               : "memory");
+}
 
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
@@ -228,6 +256,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
       const int r = q * 32 + lane;
       const float inv = 1.f / (scale[buf * TS + r] * W_SCALE);
       const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+#if ASX_DTC_EPI_FRAG
+      // 16x256b fragments straight to global: thread t of the warp holds lanes
+      // (signals) t/4 and t/4 + 8 of a 16-lane half, bins 8j + 2(t%4) + {0, 1}
+      // of a 32-bin block; each store writes 8 signals' 64-byte row segments
+      const int64_t b0 = t * TS + q * 32;
+      for (int hl = 0; hl < 2 && !(p.dbg & 2); ++hl) {
+        const uint32_t la = tmem + ((uint32_t)(q * 32 + 16 * hl) << 16);
+        const float inv0 = 1.f / (scale[buf * TS + q * 32 + 16 * hl + (lane >> 2)] * W_SCALE);
+        const float inv1 = 1.f / (scale[buf * TS + q * 32 + 16 * hl + 8 + (lane >> 2)] * W_SCALE);
+        const int64_t r0 = b0 + 16 * hl + (lane >> 2), r1 = r0 + 8;
+        for (int c0 = h * (m / 2); c0 < (h + 1) * (m / 2); c0 += 32) {
+          uint32_t re[16], im[16];
+          tmem_ld16x256(la + (uint32_t)c0, re);
+          tmem_ld16x256(la + (uint32_t)(m + c0), im);
+          tmem_wait_ld(re, im);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int bin = c0 + 8 * j + 2 * (lane & 3);
+            if (r0 < p.batch)
+              __stcs(reinterpret_cast<float4*>(p.X + r0 * 2 * p.Xs + 2 * bin),
+                     make_float4(__uint_as_float(re[4 * j]) * inv0, __uint_as_float(im[4 * j]) * inv0,
+                                 __uint_as_float(re[4 * j + 1]) * inv0, __uint_as_float(im[4 * j + 1]) * inv0));
+            if (r1 < p.batch)
+              __stcs(reinterpret_cast<float4*>(p.X + r1 * 2 * p.Xs + 2 * bin),
+                     make_float4(__uint_as_float(re[4 * j + 2]) * inv1, __uint_as_float(im[4 * j + 2]) * inv1,
+                                 __uint_as_float(re[4 * j + 3]) * inv1, __uint_as_float(im[4 * j + 3]) * inv1));
+          }
+        }
+      }
+      (void)inv;
+      (void)lane_base;
+#else
       // 16 bins per round: each thread stages its signal's 16 complex outputs,
       // then the warp writes 4 signals' 128-byte row segments per store
       float* stg = epi_stage + warp * (32 * EPI_LD);
@@ -252,6 +312,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
         }
         __syncwarp();
       }
+#endif
       tmem_fence_before();
       mbar_arrive(acc_empty);
       mbar_arrive(&sc_empty[buf]);
