@@ -418,7 +418,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   // direct form on the tensor cores (k_direct_tc): complex64 complex input,
   // N a multiple of the 32-sample K chunk, M = 128 or 256 bins (Re and Im of
   // the tile fill the 512 TMEM columns).  Cost in the same units, calibrated
-  // on config 3 (N = M = 256: 0.381 ms against the chirp path's 0.470 ms).
+  // on config 3 (N = M = 256: 0.375 ms against the chirp path's 0.470 ms).
   const char* no_dtc = std::getenv("ASX_NO_DTC");
   const bool dtc_ok = dtype == ASX_C64 && !real_input && n % 32 == 0 && (m == 128 || m == 256) &&
                       !(no_dtc && no_dtc[0] == '1');
