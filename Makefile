@@ -6,7 +6,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $(VFLAGS)
 PKG := paper_2403_16665_b200
 CSRC := $(PKG)/csrc
-UNITS := asx_api asx_launch_f32 asx_launch_f64 asx_launch_misc
+UNITS := asx_api asx_launch_f32 asx_launch_f64 asx_launch_mixed asx_launch_misc
 HDR := $(wildcard $(CSRC)/*.cuh) include/asx.h
 VNAME ?=
 BDIR := build/obj$(VNAME)

@@ -30,9 +30,6 @@
 
 #include "asx_kernels.cuh"
 
-#ifndef ASX_AFL_DBG
-#define ASX_AFL_DBG 0  // timing experiments only (wrong results): 1 no output, 2 no E1, 4 no E2, 8 no twiddle image
-#endif
 
 namespace asx {
 
@@ -147,18 +144,16 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
     // the previous signal's bins, parked by both teams long ago: write them now,
     // between this signal's butterflies and its first exchange
     mbar_wait(cx.parked, (xcnt - 1) & 1);
-    if (live_prev && !(ASX_AFL_DBG & 1)) afl_copyout(p, cx.xb0, u - stride, threadIdx.x);
+    if (live_prev) afl_copyout(p, cx.xb0, u - stride, threadIdx.x);
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
   }
   // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's output reads
   if (xcnt) mbar_wait(cx.war, (xcnt - 1) & 1);
   C* const xb = cx.xb;
-  if (!(ASX_AFL_DBG & 2)) {
 #pragma unroll
-    for (int g0 = 0; g0 < 16; ++g0) xb[t + L::RS * g0] = v[g0];
-    asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");
-  }
+  for (int g0 = 0; g0 < 16; ++g0) xb[t + L::RS * g0] = v[g0];
+  asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");
   if (CR == 0 && t == 0 && u + stride < int(p.batch)) {
     // next row: both teams started this signal together and have read it by now
     mbar_wait(cx.consumed, it & 1);
@@ -169,31 +164,23 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
                 (uint32_t)L::ROW_BYTES, cx.full);
   }
   C* rg = xb + L::RS * hi;  // this half-warp's region (g0 = hi)
-  if (!(ASX_AFL_DBG & 2)) {
 #pragma unroll
-    for (int n1 = 0; n1 < 16; ++n1) v[n1] = rg[n0 + 16 * n1];
-    __syncwarp();
-  }
+  for (int n1 = 0; n1 < 16; ++n1) v[n1] = rg[n0 + 16 * n1];
+  __syncwarp();
   // ---- S2: radix-16 over n1, × W_256^{n0 g1}
   dft_reg<16>(v);
   afl_twiddle<1>(v, cx.tbase + 64);
   // ---- E2 (half-warp): (n0, g1) -> thread (g1 = t & 15, g0)
-  if (!(ASX_AFL_DBG & 4)) {
 #pragma unroll
-    for (int g1 = 0; g1 < 16; ++g1) rg[n0 + 17 * g1] = v[g1];
-    __syncwarp();
+  for (int g1 = 0; g1 < 16; ++g1) rg[n0 + 17 * g1] = v[g1];
+  __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = rg[j + 17 * n0];
-    __syncwarp();
-  }
+  for (int j = 0; j < 16; ++j) v[j] = rg[j + 17 * n0];
+  __syncwarp();
   // ---- S3: radix-16 over n0 -> g2; park bins d = hi + 16 n0 + 256 g2 < 2048
   dft_reg<16>(v);
-  if (!(ASX_AFL_DBG & 1)) {
 #pragma unroll
-    for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(CR, hi, n0, g2)] = v[g2];
-  } else if (v[0].x == 12345.678) {
-    xb[0] = v[1];
-  }
+  for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(CR, hi, n0, g2)] = v[g2];
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(cx.parked);
 }
@@ -248,7 +235,7 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
     for (int j0 = 0; j0 < 32; j0 += 16) {
       double2 w[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) w[j] = (ASX_AFL_DBG & 8) ? mk(1.0, 0.0) : __ldg(img + L::NTH * (j0 + j));
+      for (int j = 0; j < 16; ++j) w[j] = __ldg(img + L::NTH * (j0 + j));
 #pragma unroll
       for (int j = 0; j < 16; j += 2) {
         uint32_t w8[8];
@@ -274,7 +261,7 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
   if (xcnt) {  // the last signal's bins
     const int u_last = u - stride;
     mbar_wait(cx.parked, (xcnt - 1) & 1);
-    if (u_last < batch && !(ASX_AFL_DBG & 1)) afl_copyout(p, xb0, u_last, tid);
+    if (u_last < batch) afl_copyout(p, xb0, u_last, tid);
   }
   tmem_fence_before();
   __syncthreads();

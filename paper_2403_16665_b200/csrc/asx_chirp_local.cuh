@@ -28,25 +28,6 @@
 
 #include "asx_kernels.cuh"
 
-#ifndef ASX_CL_DBG
-#define ASX_CL_DBG 0  // timing experiments only (wrong results): 1 no G1 barrier, 2 no Q4 barrier
-#endif
-#ifndef ASX_CL_P3TAB
-#define ASX_CL_P3TAB 1  // P3/Q2 twiddles from the full exact [15][16] table (else exact seeds + chain)
-#endif
-#ifndef ASX_CL_EXACTDIAG
-#define ASX_CL_EXACTDIAG 0  // diagnostic only: every P1/Q4 twiddle by FP64 sincospi (slow)
-#endif
-#ifndef ASX_CL_P1F64
-#define ASX_CL_P1F64 0  // P1/Q4 twiddles exactly rounded: W^t..W^4t kept in FP64, products on the FP64 pipe
-#endif
-#ifndef ASX_CL_P1COMP
-#define ASX_CL_P1COMP 1  // P1/Q4 twiddle products W^{4a} W^b with FMA error terms (~correctly rounded)
-#endif
-#ifndef ASX_CL_P1EXACT
-#define ASX_CL_P1EXACT 1  // P1/Q4 twiddles w, w^2, w^3 exact from TMEM (else w^2, w^3 by products)
-#endif
-
 namespace asx {
 
 struct ChirpLocal {
@@ -97,7 +78,7 @@ __device__ __forceinline__ C cmul_acc(C a, C b) {
 
 // u[r] *= w^r (r < 16) from exact w, w^2, w^3 and exact seeds w^{4a}
 // (w = {w1, w2, w3, s1, s2, s3, -, -}): every applied twiddle is one
-// (compensated with ASX_CL_P1COMP) product of exactly rounded values.
+// compensated product of exactly rounded values.
 template <typename C>
 __device__ __forceinline__ void tw16_apply(C (&u)[16], const C (&w)[8]) {
   u[1] = cmul(u[1], w[0]);
@@ -107,15 +88,9 @@ __device__ __forceinline__ void tw16_apply(C (&u)[16], const C (&w)[8]) {
   for (int a = 1; a < 4; ++a) {
     const C w4a = w[2 + a];
     u[4 * a] = cmul(u[4 * a], w4a);
-    if (ASX_CL_P1COMP) {
-      u[4 * a + 1] = cmul(u[4 * a + 1], cmul_acc(w4a, w[0]));
-      u[4 * a + 2] = cmul(u[4 * a + 2], cmul_acc(w4a, w[1]));
-      u[4 * a + 3] = cmul(u[4 * a + 3], cmul_acc(w4a, w[2]));
-    } else {
-      u[4 * a + 1] = cmul(u[4 * a + 1], cmul(w4a, w[0]));
-      u[4 * a + 2] = cmul(u[4 * a + 2], cmul(w4a, w[1]));
-      u[4 * a + 3] = cmul(u[4 * a + 3], cmul(w4a, w[2]));
-    }
+    u[4 * a + 1] = cmul(u[4 * a + 1], cmul_acc(w4a, w[0]));
+    u[4 * a + 2] = cmul(u[4 * a + 2], cmul_acc(w4a, w[1]));
+    u[4 * a + 3] = cmul(u[4 * a + 3], cmul_acc(w4a, w[2]));
   }
 }
 
@@ -159,9 +134,8 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
   for (int e = t; e < L::T2N; e += L::NT) T2[e] = exact_w<C>((e & 255) * (e / 256 + 1), 1024);
   for (int e = t; e < L::T3N; e += L::NT) {
     const int row = e / L::T3S, col = e % L::T3S;  // n'', k3
-    T3[e] = exact_w<C>(ASX_CL_P3TAB ? (col < 16 ? row * col : 0) : (col >= 1 && col <= 3 ? 4 * col * row : 0), 256);
+    T3[e] = exact_w<C>(col < 16 ? row * col : 0, 256);
   }
-  const C w1c = exact_w<C>(n16, 256);  // P3 / Q2 base twiddle W_256^{n''} (chain variant)
   if (t == 0) {
     mbar_init(stbar, 1);
     mbar_init(war, L::NT / 32);
@@ -194,22 +168,9 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       tmem_st8(tbase + j0 * WPC, wh);
       if (j0 < 8) tmem_st8(tbase + 32 + j0 * WPC, wc);
     }
-    // P1 / Q4 twiddles of W = W_16384^t: FP64 {W, W^2, W^3, W^4} (ASX_CL_P1F64),
-    // else FP32 {W, W^2, W^3, W^4, W^8, W^12} (exactly rounded)
+    // P1 / Q4 twiddles of W = W_16384^t: {W, W^2, W^3, W^4, W^8, W^12} (exactly rounded)
 #pragma unroll
-    for (int h = 0; h < 2 && ASX_CL_P1F64; ++h) {
-      uint32_t ws[8];
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int e = (2 * h + k + 1) * t;
-        double sn, cs;
-        sincospi(2.0 * double(e & (L::P - 1)) / double(L::P), &sn, &cs);
-        c_to_words(make_double2(cs, -sn), &ws[4 * k]);
-      }
-      tmem_st8(tbase + 48 + 8 * h, ws);
-    }
-#pragma unroll
-    for (int h = 0; h < 2 && !ASX_CL_P1F64; ++h) {
+    for (int h = 0; h < 2; ++h) {
       uint32_t ws[8];
 #pragma unroll
       for (int k = 0; k < CPC; ++k) {
@@ -234,63 +195,22 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
 #pragma unroll
     for (int k = 0; k < CPC; ++k) out[k] = words_to_c(&w[k * WPC], (C*)nullptr);
   };
-  // FP64 P1/Q4 twiddles: u[4a + b] *= round32(W^{4a} W^b), products in FP64
-  auto tw_p1_f64 = [&](C (&u)[16], const uint32_t (&wd)[16]) {
-    double2 w[4];  // W, W^2, W^3, W^4
-#pragma unroll
-    for (int i = 0; i < 4; ++i) w[i] = words_to_c(&wd[4 * i], (double2*)nullptr);
-    auto f32 = [](double2 d) { return mk(Real(d.x), Real(d.y)); };
-#pragma unroll
-    for (int b = 1; b < 4; ++b) u[b] = cmul(u[b], f32(w[b - 1]));
-    double2 s4 = w[3];
-#pragma unroll
-    for (int a = 1; a < 4; ++a) {
-      u[4 * a] = cmul(u[4 * a], f32(s4));
-#pragma unroll
-      for (int b = 1; b < 4; ++b) u[4 * a + b] = cmul(u[4 * a + b], f32(cmul(s4, w[b - 1])));
-      if (a < 3) s4 = cmul(s4, w[3]);
-    }
-  };
-  auto ld_p1_f64 = [&](uint32_t (&wd)[16]) {
-    uint32_t a8[8], b8[8];
-    tmem_ld8(tbase + 48, a8);
-    tmem_ld8(tbase + 56, b8);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      wd[i] = a8[i];
-      wd[8 + i] = b8[i];
-    }
-  };
   auto tw_p1 = [&](C (&w)[8]) {
     ld_tm(48, reinterpret_cast<C(&)[CPC]>(w[0]));
     ld_tm(56, reinterpret_cast<C(&)[CPC]>(w[4]));
-    if (!ASX_CL_P1EXACT) {
-      w[1] = cmul(w[0], w[0]);
-      w[2] = cmul(w[1], w[0]);
-    }
   };
   // P3 / Q2: u[k3] *= W_256^{n'' k3} from the exact shared table (or chains)
   auto tw_p3 = [&](C (&u3)[16]) {
     const C* row = T3 + L::T3S * n16;
-    if (ASX_CL_P3TAB) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        C w0, w1;
-        ld_pair(row + 2 * q, w0, w1);
-        if (q > 0) u3[2 * q] = cmul(u3[2 * q], w0);
-        u3[2 * q + 1] = cmul(u3[2 * q + 1], w1);
-      }
-    } else {
-      C w[8];
-      w[0] = w1c;
-      w[1] = cmul(w1c, w1c);
-      w[2] = cmul(w[1], w1c);
-      w[3] = row[1];
-      w[4] = row[2];
-      w[5] = row[3];
-      tw16_apply(u3, w);
+    for (int q = 0; q < 8; ++q) {
+      C w0, w1;
+      ld_pair(row + 2 * q, w0, w1);
+      if (q > 0) u3[2 * q] = cmul(u3[2 * q], w0);
+      u3[2 * q + 1] = cmul(u3[2 * q + 1], w1);
     }
   };
+
   // twiddle tables are prefetched into registers right after an exchange
   // write (the data registers are free then), i.e. inside the barrier shadow
   auto ld_t2 = [&](C (&w)[12]) {  // W_1024^{n' k2}, n' = 2 tau + (g & 1) + 128 (g >> 1), k2 = 1..3
@@ -339,19 +259,8 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     dft_reg<16>(v);
     {
       C w[8];
-      uint32_t wd[16];
-      if (ASX_CL_P1F64)
-        ld_p1_f64(wd);
-      else
-        tw_p1(w);
-      if (ASX_CL_P1F64) {
-        tw_p1_f64(v, wd);
-      } else if (ASX_CL_EXACTDIAG) {
-#pragma unroll
-        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], exact_w<C>((r * t) & (L::P - 1), L::P));
-      } else {
-        tw16_apply(v, w);
-      }
+      tw_p1(w);
+      tw16_apply(v, w);
     }
     // ---- G1: y_k1[t] -> region k1 (WAR: previous signal's Q4 reads)
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
@@ -359,7 +268,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     for (int k1 = 0; k1 < 16; ++k1) xb[k1 * L::REG + L::pos(t)] = v[k1];
     C tw2[12];
     ld_t2(tw2);
-    if (!(ASX_CL_DBG & 1)) __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
+    __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
     if (staged && t == 0 && u + stride < batch) {
       fence_proxy_async();
       mbar_expect_tx(stbar, (uint32_t)row_bytes);
@@ -444,25 +353,14 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) st_pair(rg + 2 * tau + 128 * h + L::SUB * i, v[4 * (2 * h) + i], v[4 * (2 * h + 1) + i]);
     C tw1[8];
-    uint32_t twd[16];
-    if (ASX_CL_P1F64)
-      ld_p1_f64(twd);
-    else
-      tw_p1(tw1);
-    if (!(ASX_CL_DBG & 2)) __syncthreads();
+    tw_p1(tw1);
+    __syncthreads();
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
     __syncwarp();
     if ((t & 31) == 0) mbar_arrive(war);
     ++xcnt;
-    if (ASX_CL_P1F64) {
-      tw_p1_f64(v, twd);
-    } else if (ASX_CL_EXACTDIAG) {
-#pragma unroll
-      for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], exact_w<C>((r * t) & (L::P - 1), L::P));
-    } else {
-      tw16_apply(v, tw1);
-    }
+    tw16_apply(v, tw1);
     dft_reg<16>(v);
     {
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;

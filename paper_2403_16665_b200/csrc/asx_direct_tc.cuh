@@ -36,8 +36,9 @@
 
 #include "asx_engine.cuh"
 
-#ifndef ASX_DTC_EPI_FRAG
-#define ASX_DTC_EPI_FRAG 1  // epilogue: 16x256b TMEM fragments straight to global (0: 32x32b + smem transpose)
+#ifndef ASX_DTC_ABLATE
+#define ASX_DTC_ABLATE 0  // timing-only ablation builds (`make variant`, wrong results): 1 no MMAs, 2 no
+                          // epilogue drain, 4 no x loads in the converters.  0 in the shipped library.
 #endif
 
 namespace asx {
@@ -53,12 +54,9 @@ constexpr int A_STAGE = 4 * A_TERM;        // [Ar hi | Ar lo | Ai hi | Ai lo]
 constexpr int MMAX = 256;                  // bins per tile (MMA N)
 constexpr int B_STAGE = 2 * MMAX * KC * 2; // one part (Wr or Wi) [hi | lo] at M = 256: 32 KB
 constexpr int NA = 2, NB = 3;
-constexpr int EPI_LD = 36;                 // staging row stride (floats): 16 bins + pad, conflict-free
-constexpr int EPI_WARP = 32 * EPI_LD * 4;  // per-warp output staging: 4.5 KB
 constexpr float W_SCALE = 256.0f;
 constexpr int SMEM_BYTES =
-    1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 512 /*bars, slot*/ + 2 * TS * 4 /*scales*/ +
-    (ASX_DTC_EPI_FRAG ? 0 : 8 * EPI_WARP);
+    1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 512 /*bars, slot*/ + 2 * 2 * TS * 4 /*scales*/;
 constexpr int TMEM_COLS = 512;
 
 struct Params {
@@ -69,8 +67,6 @@ struct Params {
   int64_t batch;
   int n, m;         // n % 32 == 0; m in {128, 256}
   const unsigned char* wimg;  // plan-time image: [chunk][Wr | Wi][hi | lo][m][32] fp16, swizzled
-  int dbg;          // timing-only ablations (env ASX_DTC_DBG, wrong results): 1 no MMAs, 2 no epilogue
-                    // drain, 4 no x loads in the converters
 };
 
 // byte offset of element (row, k) in a K-major SWIZZLE_64B tile of 32-wide fp16
@@ -172,8 +168,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   uint64_t* sc_full = acc_empty + 1;   // 2, count NSCALE
   uint64_t* sc_empty = sc_full + 2;    // 2, count NCONV
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_empty + 2);
-  float* scale = reinterpret_cast<float*>(sB + NB * B_STAGE + 512);  // [2][TS]
-  float* epi_stage = scale + 2 * TS;                                   // 8 x [32][EPI_LD]
+  // per-signal power-of-two scale 2^e as two factors 2^e1 * 2^e2 (each in the
+  // normal float range for any e the fp32 input range produces): [2 bufs][TS][2]
+  float2* scale = reinterpret_cast<float2*>(sB + NB * B_STAGE + 512);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kcn = p.n / KC;                 // K chunks
@@ -214,13 +211,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     auto convert = [&](int64_t t, int buf, int c) {
       const uint32_t s = ca % NA;
       float4 v[4][2];
-      const float* sc = scale + buf * TS;
+      const float2* sc = scale + buf * TS;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
         const int64_t b = t * TS + row;
         v[i][0] = v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b < p.batch && !(p.dbg & 4)) {
+        if (b < p.batch && !(ASX_DTC_ABLATE & 4)) {
           const float4* src = reinterpret_cast<const float4*>(p.x + b * 2 * p.xs + (int64_t)c * 2 * KC) + 2 * g;
           v[i][0] = __ldcs(src);
           v[i][1] = __ldcs(src + 1);
@@ -231,12 +228,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
-        const float f = sc[row];
+        const float2 f = sc[row];
         uint2 rh, rl, ih, il;
-        split2(v[i][0].x * f, v[i][0].z * f, rh.x, rl.x);
-        split2(v[i][1].x * f, v[i][1].z * f, rh.y, rl.y);
-        split2(v[i][0].y * f, v[i][0].w * f, ih.x, il.x);
-        split2(v[i][1].y * f, v[i][1].w * f, ih.y, il.y);
+        split2(v[i][0].x * f.x * f.y, v[i][0].z * f.x * f.y, rh.x, rl.x);
+        split2(v[i][1].x * f.x * f.y, v[i][1].z * f.x * f.y, rh.y, rl.y);
+        split2(v[i][0].y * f.x * f.y, v[i][0].w * f.x * f.y, ih.x, il.x);
+        split2(v[i][1].y * f.x * f.y, v[i][1].w * f.x * f.y, ih.y, il.y);
         const uint32_t off = swz(row, 4 * g);
         *reinterpret_cast<uint2*>(st + off) = rh;
         *reinterpret_cast<uint2*>(st + A_TERM + off) = rl;
@@ -253,18 +250,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
       mbar_wait(acc_full, ntile_done & 1);
       tmem_fence_after();
       const int q = warp & 3, h = warp >> 2;
-      const int r = q * 32 + lane;
-      const float inv = 1.f / (scale[buf * TS + r] * W_SCALE);
-      const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-#if ASX_DTC_EPI_FRAG
       // 16x256b fragments straight to global: thread t of the warp holds lanes
       // (signals) t/4 and t/4 + 8 of a 16-lane half, bins 8j + 2(t%4) + {0, 1}
       // of a 32-bin block; each store writes 8 signals' 64-byte row segments
       const int64_t b0 = t * TS + q * 32;
-      for (int hl = 0; hl < 2 && !(p.dbg & 2); ++hl) {
+      for (int hl = 0; hl < 2 && !(ASX_DTC_ABLATE & 2); ++hl) {
         const uint32_t la = tmem + ((uint32_t)(q * 32 + 16 * hl) << 16);
-        const float inv0 = 1.f / (scale[buf * TS + q * 32 + 16 * hl + (lane >> 2)] * W_SCALE);
-        const float inv1 = 1.f / (scale[buf * TS + q * 32 + 16 * hl + 8 + (lane >> 2)] * W_SCALE);
+        // exact inverse of 2^e1 * 2^e2 * W_SCALE, again as two normal factors
+        const float2 s0 = scale[buf * TS + q * 32 + 16 * hl + (lane >> 2)];
+        const float2 s1 = scale[buf * TS + q * 32 + 16 * hl + 8 + (lane >> 2)];
+        const float inv0a = 1.f / s0.x, inv0b = 1.f / (s0.y * W_SCALE);
+        const float inv1a = 1.f / s1.x, inv1b = 1.f / (s1.y * W_SCALE);
         const int64_t r0 = b0 + 16 * hl + (lane >> 2), r1 = r0 + 8;
         for (int c0 = h * (m / 2); c0 < (h + 1) * (m / 2); c0 += 32) {
           uint32_t re[16], im[16];
@@ -276,43 +272,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
             const int bin = c0 + 8 * j + 2 * (lane & 3);
             if (r0 < p.batch)
               __stcs(reinterpret_cast<float4*>(p.X + r0 * 2 * p.Xs + 2 * bin),
-                     make_float4(__uint_as_float(re[4 * j]) * inv0, __uint_as_float(im[4 * j]) * inv0,
-                                 __uint_as_float(re[4 * j + 1]) * inv0, __uint_as_float(im[4 * j + 1]) * inv0));
+                     make_float4(__uint_as_float(re[4 * j]) * inv0a * inv0b, __uint_as_float(im[4 * j]) * inv0a * inv0b,
+                                 __uint_as_float(re[4 * j + 1]) * inv0a * inv0b,
+                                 __uint_as_float(im[4 * j + 1]) * inv0a * inv0b));
             if (r1 < p.batch)
               __stcs(reinterpret_cast<float4*>(p.X + r1 * 2 * p.Xs + 2 * bin),
-                     make_float4(__uint_as_float(re[4 * j + 2]) * inv1, __uint_as_float(im[4 * j + 2]) * inv1,
-                                 __uint_as_float(re[4 * j + 3]) * inv1, __uint_as_float(im[4 * j + 3]) * inv1));
+                     make_float4(__uint_as_float(re[4 * j + 2]) * inv1a * inv1b,
+                                 __uint_as_float(im[4 * j + 2]) * inv1a * inv1b,
+                                 __uint_as_float(re[4 * j + 3]) * inv1a * inv1b,
+                                 __uint_as_float(im[4 * j + 3]) * inv1a * inv1b));
           }
         }
       }
-      (void)inv;
-      (void)lane_base;
-#else
-      // 16 bins per round: each thread stages its signal's 16 complex outputs,
-      // then the warp writes 4 signals' 128-byte row segments per store
-      float* stg = epi_stage + warp * (32 * EPI_LD);
-      const int64_t b0 = t * TS + q * 32;
-      for (int c0 = h * (m / 2); c0 < (h + 1) * (m / 2) && !(p.dbg & 2); c0 += 16) {
-        uint32_t re[16], im[16];
-        tmem_ld16(lane_base + (uint32_t)c0, re);
-        tmem_ld16(lane_base + (uint32_t)(m + c0), im);
-        tmem_wait_ld();
-        float4* srow = reinterpret_cast<float4*>(stg + lane * EPI_LD);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          srow[i] = make_float4(__uint_as_float(re[2 * i]) * inv, __uint_as_float(im[2 * i]) * inv,
-                                __uint_as_float(re[2 * i + 1]) * inv, __uint_as_float(im[2 * i + 1]) * inv);
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rr = 4 * i + (lane >> 3), j = lane & 7;
-          const int64_t bb = b0 + rr;
-          const float4 v = reinterpret_cast<const float4*>(stg + rr * EPI_LD)[j];
-          if (bb < p.batch) __stcs(reinterpret_cast<float4*>(p.X + bb * 2 * p.Xs + 2 * c0) + j, v);
-        }
-        __syncwarp();
-      }
-#endif
       tmem_fence_before();
       mbar_arrive(acc_empty);
       mbar_arrive(&sc_empty[buf]);
@@ -357,7 +328,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
             for (int k = 0; k < KC / 16; ++k) {
               const uint32_t ko = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
               const uint64_t Bh = sdesc(bh + ko), Bl = sdesc(bl + ko);
-              if (p.dbg & 1) {
+              if (ASX_DTC_ABLATE & 1) {
               } else if (part == 0) {  // Re += Ar Wr,  Im += Ai Wr
                 const uint32_t first = (c == 0 && k == 0) ? 0u : 1u;
                 mma_f16(d_re, sdesc(arh + ko), Bh, id, first);
@@ -394,7 +365,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
       mbar_wait(&sc_empty[buf], ((it >> 1) & 1) ^ 1);
-      float* sc = scale + buf * TS;
+      float2* sc = scale + buf * TS;
       for (int r0 = sw * (TS / (NSCALE / 32)); r0 < (sw + 1) * (TS / (NSCALE / 32)); r0 += 4) {
         float mx[4] = {0.f, 0.f, 0.f, 0.f};
         const int nq = p.n / 2;  // float4 per row
@@ -422,9 +393,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], o));
           if (lane == rr) {
-            float sv = 1.f;
-            if (mx[rr] > 0.f && mx[rr] <= 3.0e38f) sv = exp2f((float)(10 - ilogbf(mx[rr])));
-            sc[r0 + rr] = sv;
+            // 2^e with e = 10 - ilogb(max|x|) in [-117, 159] over the finite
+            // fp32 range (subnormals included), split e = e1 + e2 so both
+            // factors and their inverses (times W_SCALE) stay normal floats
+            int e = 0;
+            if (mx[rr] > 0.f && mx[rr] <= 3.402823466e38f) e = 10 - ilogbf(mx[rr]);
+            const int e1 = e / 2;
+            sc[r0 + rr] = make_float2(exp2f((float)e1), exp2f((float)(e - e1)));
           }
         }
       }

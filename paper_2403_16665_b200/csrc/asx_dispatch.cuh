@@ -11,7 +11,6 @@
 
 #include "../../include/asx.h"
 #include "asx_afft_local.cuh"
-#include "asx_chirp2h.cuh"
 #include "asx_chirp_local.cuh"
 #include "asx_chirp_local128.cuh"
 #include "asx_large.cuh"
@@ -87,15 +86,18 @@ cudaError_t prep_smem(KernelT kern, size_t smem) {
   return cudaSuccess;
 }
 
-template <typename Real, int P, int KIND>
+// IO: element type of the signals / bins when it differs from the arithmetic
+// type (complex64 α-FFT plans: IO = float, Real = double).
+template <typename Real, int P, int KIND, typename IO = Real>
 cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const LaunchEnv& env) {
   using G = Cfg<P, Real>;
+  constexpr bool SAME_IO = sizeof(IO) == sizeof(Real);
   constexpr int KR = KIND == KIND_AFFT ? G::KR : 1;
   constexpr bool DBUF = persist_dbuf<Real, P, G::NT, KIND>();
   using L = PersistLayout<Real, P, G::NT, G::TPB, false, KR, DBUF>;
   if (batch == 0) return cudaSuccess;
-  const size_t row_bytes = size_t(kp.n) * (kp.real_in ? sizeof(Real) : 2 * sizeof(Real));
-  auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR>;
+  const size_t row_bytes = size_t(kp.n) * (kp.real_in ? sizeof(IO) : 2 * sizeof(IO));
+  auto kern = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR, false, false, IO>;
   // one-time opt-in to the full shared-memory carve-out for this kernel
   static thread_local int attr_set_for = -1;
   int dev = 0;
@@ -127,7 +129,8 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
     return c.per_sm;
   };
   if (G::NT == 1) kp.staged = 0;
-  if constexpr (KIND == KIND_AFFT && G::NT == 512 && sizeof(Real) == 4 && size_t(P) * 2 * sizeof(Real) <= 65536) {
+  if constexpr (SAME_IO && KIND == KIND_AFFT && G::NT == 512 && sizeof(Real) == 4 &&
+                size_t(P) * 2 * sizeof(Real) <= 65536) {
     // two 512-thread teams per CTA split one signal's residues, one TMA-staged row
     // (complex64 P = 8192: config 4 alpha-FFT 19.2 -> 17.5 ms; complex128 P = 4096
     // measured slower than two independent CTAs per SM: 0.260 vs 0.242 ms)
@@ -154,7 +157,7 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
       return cudaGetLastError();
     }
   }
-  if constexpr (KIND == KIND_AFFT && sizeof(Real) == 8 && P == AfftLocal::P) {
+  if constexpr (SAME_IO && KIND == KIND_AFFT && sizeof(Real) == 8 && P == AfftLocal::P) {
     // group-local α-FFT kernel (asx_afft_local.cuh): one CTA (two residue teams) per SM
     if (env.use_afl && kp.r == 2 && kp.fold == 1 && !kp.real_in && kp.n == P && kp.m <= P && kp.staged &&
         kp.afl && batch < (int64_t(1) << 31) && AfftLocal::SMEM <= env.smem_optin) {
@@ -285,7 +288,7 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
   }
   if constexpr (KIND == KIND_AFFT && KR == 1) {
     if (rsplit) {
-      auto kern_rs = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR, false, true>;
+      auto kern_rs = k_fft_persist<Real, P, G::NT, G::TPB, KIND, G::MINB, false, KR, false, true, IO>;
       static thread_local int rs_attr_for = -1;
       if (rs_attr_for != dev) {
         cudaError_t e = cudaFuncSetAttribute(kern_rs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
@@ -423,17 +426,12 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <typename Real, int Q, int NT>
-auto chirp2h_kernel() {
-  return k_chirp2h<Real, Q, NT>;
-}
-
-
 cudaError_t launch_large(int dbl, int64_t P1, int mode_cols, int mode_rows, int which, const LParams& lp,
                          cudaStream_t st);
-int chirp2h_occupancy(int dbl);
-cudaError_t launch_chirp2h(int dbl, const KParams& kp, int grid, void* scratch, const void* cw, const void* cwc,
-                           cudaStream_t st);
+
+// complex64 α-FFT plans: the FP64 recursion with complex64 loads / stores
+// (asx_launch_mixed.cu)
+cudaError_t launch_afft_io32(int P, const KParams& kp, int64_t batch, cudaStream_t st, const LaunchEnv& env);
 
 extern template cudaError_t launch_by_size<float>(int, int, const KParams&, int64_t, cudaStream_t, const LaunchEnv&);
 extern template cudaError_t launch_by_size<double>(int, int, const KParams&, int64_t, cudaStream_t, const LaunchEnv&);

@@ -66,6 +66,15 @@ __device__ __forceinline__ C load_row(const unsigned char* stage, const void* x,
   return load_in<C>(x, row_off + n, real_in);
 }
 
+// complex value converted to another precision (identity when equal)
+template <typename To, typename From>
+__device__ __forceinline__ To widen(From v) {
+  if constexpr (sizeof(To) == sizeof(From))
+    return v;
+  else
+    return mk(decltype(To{}.x)(v.x), decltype(To{}.x)(v.y));
+}
+
 // Compiler-only fence: keeps the scheduler from hoisting every table load of an
 // unrolled loop at once (which would double live registers and spill).
 __device__ __forceinline__ void reg_fence() { asm volatile("" ::: "memory"); }
@@ -149,10 +158,15 @@ struct TmemCfg {
 // serves them all, so a CTA of TPB teams keeps staging at full occupancy.
 // RS (α-FFT, small batches): the work unit is one (signal, residue) pair
 // instead of a signal, so one signal's r residues run on r teams at once.
+// IO (α-FFT only): the element type of x and X when it differs from the
+// arithmetic type Real (complex64 plans run the recursion in FP64: samples are
+// widened on load, bins rounded once on store).
 template <typename Real, int P, int NT, int TPB, int KIND, int MINB, bool TM = false, int KR = 1, bool SPLIT = false,
-          bool RS = false>
+          bool RS = false, typename IO = Real>
 __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   static_assert(!SPLIT || (KIND == 0 && NT > 32), "SPLIT: alpha-FFT with CTA-wide team barriers");
+  static_assert(KIND == 0 || sizeof(IO) == sizeof(Real), "mixed precision: alpha-FFT only");
+  using CI = typename CT<IO>::T;
   constexpr bool TS = TM && KIND == KIND_CHIRP;  // last-pass twiddle seeds in TMEM too
   constexpr bool DBUF = persist_dbuf<Real, P, NT, KIND>();
   using E = Fft<Real, P, NT, ASX_TWTAB_MAX, TS, DBUF>;
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int team = threadIdx.x / NT, t = threadIdx.x % NT;
   const bool staged = p.staged != 0;
-  const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(Real) : sizeof(C));
+  const size_t row_bytes = size_t(p.n) * (p.real_in ? sizeof(IO) : sizeof(CI));
   C* fbuf = reinterpret_cast<C*>(smraw) + team * KR * E::SMEM_ELEMS;
   const int steam = SPLIT ? 0 : team;  // owner of the staged row / its mbarrier
   unsigned char* stage = smraw + L::FFT_BYTES + steam * L::stage_bytes(row_bytes, staged);
@@ -357,9 +371,9 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
             const int nn = t + NT * i;
             C val = mk(Real(0), Real(0));
             if (live && c < p.r) {
-              val = load_row<C>(stage, p.x, row_off, nn, p.real_in, staged);
+              val = widen<C>(load_row<CI>(stage, p.x, row_off, nn, p.real_in, staged));
               for (int s = 1; s < p.fold; ++s)
-                val = cadd(val, load_row<C>(stage, p.x, row_off, nn + int64_t(s) * P, p.real_in, staged));
+                val = cadd(val, widen<C>(load_row<CI>(stage, p.x, row_off, nn + int64_t(s) * P, p.real_in, staged)));
             }
             if (c != 0) {
               if (i > 0) wc = ((i % ASX_AFFT_RESEED) == 0) ? tw_lookup_rt(twa, c * nn, p.lfA) : cmul(wc, wst);
@@ -383,7 +397,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
         }
         E::template run<KR>(v, fbuf, t, tr, xs);
         if (live) {
-          C* X = reinterpret_cast<C*>(p.X) + int64_t(sig(u)) * p.Xs;
+          CI* X = reinterpret_cast<CI*>(p.X) + int64_t(sig(u)) * p.Xs;
           const int64_t period = p.r * P;
 #pragma unroll
           for (int k = 0; k < KR; ++k) {
@@ -392,7 +406,7 @@ __global__ void __launch_bounds__(NT* TPB, MINB) k_fft_persist(KParams p) {
 #pragma unroll
             for (int i = 0; i < R; ++i) {
               const int d = t + NT * i;
-              for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = v[k][i];
+              for (int64_t mm = c + p.r * d; mm < p.m; mm += period) X[mm] = widen<CI>(v[k][i]);
             }
           }
         }

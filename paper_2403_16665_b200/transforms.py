@@ -172,12 +172,17 @@ class Plan:
         return (_NP_REAL if self.real_input else _NP_COMPLEX)[self._dtype]
 
     def execute(self, x, out=None, stream=None):
-        """Batched transform of a CUDA tensor x (B, N) or (N,) -> (B, M) / (M,)."""
+        """Batched transform of a CUDA tensor x (..., N) -> (..., M); rows are signals.
+
+        Leading dimensions are flattened into the batch and restored on the
+        output (``out``, if given, must then be a (B, M) view with B their
+        product)."""
         torch = _torch()
-        squeeze = x.dim() == 1
-        xb = x.unsqueeze(0) if squeeze else x
-        if xb.shape[-1] != self.n:
+        if x.dim() == 0 or x.shape[-1] != self.n:
             raise ValueError(f"plan is for N={self.n}, got {tuple(x.shape)} samples")
+        lead = tuple(x.shape[:-1])
+        squeeze = x.dim() == 1
+        xb = x.unsqueeze(0) if squeeze else (x.reshape(-1, self.n) if x.dim() > 2 else x)
         want = getattr(torch, np.dtype(self._in_dtype()).name)
         xb = xb.resolve_conj().resolve_neg()  # lazy conj/neg views would hand the kernel raw memory
         if xb.dtype != want:
@@ -199,14 +204,17 @@ class Plan:
         Xs = out.stride(0) if batch > 1 else self.m
         _lib.check(_lib.lib().asx_execute(self._handle, xb.data_ptr(), xs, out.data_ptr(), Xs, batch, st),
                    "execute")
-        return out[0] if squeeze else out
+        if squeeze:
+            return out[0]
+        return out.view(lead + (self.m,)) if len(lead) > 1 else out
 
     def execute_host(self, x, out=None, chunk: int = 0) -> np.ndarray:
         """Batched transform of a host array (B, N) or (N,); copies run inside the C ABI."""
         arr = np.asarray(x)
-        squeeze = arr.ndim == 1
-        if arr.shape[-1] != self.n:
+        if arr.ndim == 0 or arr.shape[-1] != self.n:
             raise ValueError(f"plan is for N={self.n}, got {arr.shape} samples")
+        lead = arr.shape[:-1]
+        squeeze = arr.ndim == 1
         arr = np.ascontiguousarray(arr.reshape(-1, self.n), dtype=self._in_dtype())
         batch = arr.shape[0]
         if out is None:
@@ -216,7 +224,9 @@ class Plan:
         _lib.check(_lib.lib().asx_execute_host(self._handle, arr.ctypes.data, self.n, out.ctypes.data,
                                                self.m, batch, int(chunk)), "execute_host")
         out = out.reshape(batch, self.m)
-        return out[0] if squeeze else out
+        if squeeze:
+            return out[0]
+        return out.reshape(lead + (self.m,)) if len(lead) > 1 else out
 
     def __call__(self, x, **kw):
         return self.execute(x, **kw) if _is_tensor(x) and x.device.type == "cuda" else self.execute_host(x, **kw)
@@ -291,11 +301,11 @@ def transform_samples(x, p: Plan, counter: OpCounter | None = None):
     x: (N,) or (B, N) numpy array -> numpy bins; CUDA tensor -> CUDA tensor.
     """
     shape = tuple(x.shape)
-    if len(shape) not in (1, 2) or shape[-1] != p.n:
+    if not shape or shape[-1] != p.n:
         got = shape[0] if len(shape) == 1 else shape
         raise ValueError(f"plan is for N={p.n}, got {got} samples")
     out = p(x)
-    _count(counter, p, 1 if len(shape) == 1 else shape[0])
+    _count(counter, p, int(np.prod(shape[:-1])) if len(shape) > 1 else 1)
     return out
 
 

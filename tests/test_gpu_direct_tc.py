@@ -125,3 +125,46 @@ def test_linearity(asx):
     gx, gy = _run(asx, x, n, a, d, m), _run(asx, y, n, a, d, m)
     gs = _run(asx, (x + 2 * y).astype(np.complex64), n, a, d, m)
     assert orc.rel_err(gs, gx + 2 * gy) <= 4 * TOL
+
+
+def test_scale_at_the_edges_of_the_float_range(asx):
+    """Per-signal scaling over the whole finite fp32 range: subnormal and
+    near-FLT_MAX amplitudes, where a single-factor 2^e scale overflows
+    (2^e > FLT_MAX for max|x| < 2^-117) or the fp16 split overflows."""
+    n, a, d, m = 256, 37, 100, 256
+    rng = np.random.default_rng(21)
+    amp = np.array([1e-35, 1e-38, 1e-40, 1e-44, 3.3e38 / 4096.0, 1e36, 1.0, 5e-39] * 16)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(amp.size)]) * amp[:, None]
+    x = x.astype(np.complex64)
+    got = _run(asx, x, n, a, d, m)
+    assert _variant() == VARIANT_DTC
+    want = orc.direct(x.astype(np.complex128), a, d, m)
+    assert np.all(np.isfinite(got))
+    # |X| <= N max|x| stays finite in fp32 for these amplitudes; subnormal
+    # inputs carry fewer than 24 significant bits, so the bound is taken
+    # against their own (exactly represented) values, row by row
+    for i in range(amp.size):
+        if amp[i] >= 1e-37:
+            assert orc.rel_err(got[i:i + 1], want[i:i + 1]) <= TOL, (i, amp[i])
+        else:
+            scale = np.max(np.abs(want[i]))
+            assert np.max(np.abs(got[i] - want[i])) <= max(TOL * scale, 1e-44 * n), (i, amp[i])
+
+
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_long_signals_at_the_cap(asx, n):
+    """The longest K the tensor-core form takes (N <= 4096; longer plans use
+    chirp-z): tone signals, fp32 TMEM accumulation over 4096 terms."""
+    a, d, m = 1, 16, 256
+    t = np.arange(n)
+    rng = np.random.default_rng(n)
+    rows = []
+    for _ in range(256):
+        f = rng.uniform(1, n / 16 - 1, 2)
+        rows.append(sum(np.exp(2j * np.pi * fk * t / n) for fk in f) + 0.01 * orc.unit_disk(rng, n))
+    x = np.stack(rows).astype(np.complex64)
+    got = _run(asx, x, n, a, d, m)
+    assert _variant() == VARIANT_DTC
+    assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
+    p = asx.plan(8192, asx.DenseFactor(d, a), m=m, dtype="complex64", method="auto")
+    assert p.method != "direct" or n <= 4096

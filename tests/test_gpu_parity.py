@@ -368,3 +368,39 @@ def test_four_step_reentrant_across_streams(asx, torch):
     assert torch.equal(got, want)
     host = p.execute_host(x, chunk=1)  # six chunks over the three-stream ring
     np.testing.assert_array_equal(host, want.cpu().numpy())
+
+
+def test_complex64_fft_is_fp64_inside(asx, torch):
+    # the α-FFT recursion of a complex64 plan runs in FP64: its
+    # error is the complex64 output rounding only, far below the bound even on
+    # signals whose energy lies outside the M-bin window (config 4's hard case)
+    n = 8192
+    t = np.arange(n)
+    rng = np.random.default_rng(77)
+    rows = []
+    for _ in range(4):  # tones at f > N/8: none falls inside the alpha = 1/8 window
+        f = rng.uniform(n / 8 + 50, n / 2 - 50, 4)
+        ph = rng.uniform(0, 2 * np.pi, 4)
+        sig = sum(np.exp(2j * np.pi * fk * t / n + 1j * pk) for fk, pk in zip(f, ph))
+        rows.append(sig + 0.1 * (rng.standard_normal(n) + 1j * rng.standard_normal(n)))
+    x = np.stack(rows).astype(np.complex64)
+    want = orc.direct(x.astype(np.complex128), 1, 8, n)
+    got, p = gpu_run(asx, x, 1, 8, n, "fft", dtype="complex64")
+    assert p.method == "fft"
+    assert orc.rel_err(got, want) <= 1e-6
+    # the FP64 engine's inner size limit applies to complex64 plans too
+    with pytest.raises(asx.UnsupportedSizeError):
+        asx.plan(16384, asx.DenseFactor(1), m=16384, dtype="complex64", method="fft")
+
+
+def test_leading_dims_flatten_into_the_batch(asx, torch):
+    rng = np.random.default_rng(9)
+    x = np.stack([orc.unit_disk(rng, 256) for _ in range(6)]).reshape(2, 3, 256)
+    want = orc.direct(x.reshape(6, 256), 1, 2, 256).reshape(2, 3, 256)
+    p = asx.plan(256, asx.DenseFactor(2), m=256, method="fft")
+    got = p.execute(torch.from_numpy(x).cuda())
+    assert tuple(got.shape) == (2, 3, 256)
+    assert orc.rel_err(got.cpu().numpy().reshape(6, 256), want.reshape(6, 256)) <= TOL64
+    got_h = p.execute_host(x)
+    assert got_h.shape == (2, 3, 256)
+    assert orc.rel_err(got_h.reshape(6, 256), want.reshape(6, 256)) <= TOL64
