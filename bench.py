@@ -4,13 +4,20 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--method auto]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
-    python bench.py --impl reference      # the reference CPU path (oracle port) on host cores
+    python bench.py --impl reference      # the reference's own CPU path on host cores
 
 Workload: BASELINE config 4 by default (65536 signals x N=8192 complex64,
 α = 1/8, M = N), the config the metric is quoted on at 1/2/4/8 GPUs; the
 batch is split into contiguous shards, one per rank, with no communication in
 the timed region (strong scaling of a fixed total batch).  A step is one
 transform of the rank's whole shard.  Rank 0 prints ONE JSON line.
+
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL); under torchrun
+the world size must equal N.  After the timed region every rank checks ALL
+of its shard's bins against the complex128 GPU path (a different algorithm)
+on the same inputs and the per-signal max|ΔX|/max|X| is all-reduced (MAX)
+into the line's ``parity`` field.
 """
 
 from __future__ import annotations
@@ -48,11 +55,35 @@ def parse_args():
                     help="skip the side measurements of configs 1a, 1b and 3 (not part of value)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target busy seconds per host core for the CPU baseline sample")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend for N > 1 (gloo lets several ranks share one GPU in tests)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-run parity check")
+    ap.add_argument("--ref-step-seconds", type=float, default=2.0,
+                    help="--impl reference: target wall seconds of one step (a bounded sample)")
     return ap.parse_args()
 
 
+def maybe_self_launch(args) -> None:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run, N ranks."""
+    if "WORLD_SIZE" in os.environ:
+        ws = int(os.environ["WORLD_SIZE"])
+        if ws != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 from paper_2403_16665_b200.dist import barrier as dist_barrier  # noqa: E402
-from paper_2403_16665_b200.dist import gather_checksums, max_over_ranks, shard_range  # noqa: E402
+from paper_2403_16665_b200.dist import gather_checksums, max_over_ranks, shard_range, sum_over_ranks  # noqa: E402
 from paper_2403_16665_b200.dist import world as dist_env  # noqa: E402
 
 
@@ -204,54 +235,143 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU reference
+#
+# The reference package, installed unmodified into baseline/_ref (DESIGN.md
+# §6: pip install --no-index --no-deps --target baseline/_ref), timed through
+# its own public API: fastpath.transform_samples with a pre-built plan, one
+# signal per call as the reference's batching is a Python loop
+# (ref/fastpath.py:162-181; plan construction untimed, ref/bench.py:14-16).
+# Configs the reference cannot run (config 3: alpha*N not an integer; config
+# 1b: alpha_ref = 10 has no power-of-two plan, its route is naive_forward)
+# use the reference's naive_forward when it accepts the pair, else the CPU
+# oracle port (kind "port").
 
-def _cpu_worker(args):
-    key, lo, hi = args
-    import numpy as np
-
-    from oracle import alpha_oracle as orc  # CPU baseline leg only
-    from paper_2403_16665_b200.signals import WORKLOADS, generate
-
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    w = WORKLOADS[key]
-    x = generate(w, lo, hi - lo, threads=1).astype(np.complex128)
-    a, d = w.alpha.numerator, w.alpha.denominator
-    t0 = time.perf_counter()
-    for row in x:  # one signal per call, as the reference's transform_samples
-        if a == 1 and (w.n & (w.n - 1)) == 0:
-            orc.alpha_fft(row[None], a, d, w.m)
-        else:
-            orc.direct(row[None], a, d, w.m)
-    return time.perf_counter() - t0, hi - lo
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
 
 
-def cpu_reference(key: str, target_seconds: float):
-    """The reference's CPU path (oracle port of transform_samples / naive_forward)
-    on this host's cores, over a bounded seeded sample of the workload."""
-    import multiprocessing as mp
+def _ref_module():
+    if os.path.isdir(os.path.join(REF_DIR, "alpha_spectra")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import alpha_spectra
 
+        return alpha_spectra
+    return None
+
+
+def _ref_callable(key: str):
+    """(kind, fn(row) -> bins[:M]) of the reference's CPU path for a workload."""
     from paper_2403_16665_b200.signals import WORKLOADS
 
     w = WORKLOADS[key]
-    cores = len(os.sched_getaffinity(0))
-    # calibrate on a few signals, then size the sample to ~target_seconds of
-    # busy time on every core (cores * target_seconds CPU-seconds in total)
-    dt, k = _cpu_worker((key, 0, 4))
-    per = max(dt / k, 1e-5)
-    sample = int(max(cores, min(w.batch, cores * target_seconds / per)))
-    sample = max(cores, (sample // cores) * cores)
-    chunks = [(key, i * sample // cores, (i + 1) * sample // cores) for i in range(cores)]
-    ctx = mp.get_context("fork")
+    a, d = w.alpha.numerator, w.alpha.denominator  # BASELINE alpha = a/d = 1 / DenseFactor(d, a)
+    ref = _ref_module()
+    if ref is not None and (w.n * d) % a == 0:
+        from alpha_spectra import fastpath, oracle
+        from alpha_spectra.core import DenseFactor, Signal
+
+        density = DenseFactor(d, a)
+        try:
+            pl = fastpath.plan(w.n, density)  # untimed, as the reference's bench
+            return "reference", "alpha_spectra.fastpath.transform_samples", \
+                lambda row: fastpath.transform_samples(row, pl)[: w.m]
+        except ValueError:
+            return "reference", "alpha_spectra.oracle.naive_forward", \
+                lambda row: oracle.naive_forward(Signal(row), density).bins[: w.m]
+    from oracle import alpha_oracle as orc  # CPU baseline leg only: the port, when the reference cannot run
+
+    if a == 1 and (w.n & (w.n - 1)) == 0:
+        return "port", "oracle/alpha_oracle.py alpha_fft (restated transform_samples)", \
+            lambda row: orc.alpha_fft(row[None], a, d, w.m)[0]
+    return "port", "oracle/alpha_oracle.py direct (restated naive_forward, generalised alpha)", \
+        lambda row: orc.direct(row[None], a, d, w.m)[0]
+
+
+_POOL_STATE = {}
+
+
+def _pool_init(key, lo_hi):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import numpy as np
+
+    from paper_2403_16665_b200.signals import WORKLOADS, generate
+
+    _POOL_STATE["fn"] = _ref_callable(key)[2]
+    _POOL_STATE["key"] = key
+    _POOL_STATE["np"] = np
+    _POOL_STATE["gen"] = lambda lo, hi: generate(WORKLOADS[key], lo, hi - lo, threads=1).astype(np.complex128)
+
+
+def _pool_step(lo_hi):
+    """One worker's share of a step: its signals, one reference call each; busy seconds."""
+    lo, hi = lo_hi
+    x = _POOL_STATE.get(("x", lo, hi))
+    if x is None:
+        x = _POOL_STATE["gen"](lo, hi)  # generated once per worker slice, untimed
+        _POOL_STATE[("x", lo, hi)] = x
+    fn = _POOL_STATE["fn"]
     t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_cpu_worker, chunks)
-    wall = time.perf_counter() - t0
-    busy = max(r[0] for r in res)
-    value = sample * w.m / busy
-    return {"value": value, "unit": "complex points/s", "cores": cores, "kind": "port",
-            "sample": f"{sample} of {w.batch} signals of config {key} (per-signal oracle port of "
-                      f"ref transform_samples/naive_forward, {cores} processes, {busy:.2f} s busy per "
-                      f"process, {sum(r[0] for r in res):.1f} CPU-s in total, {wall:.2f} s wall)"}
+    for row in x:
+        fn(row)
+    return time.perf_counter() - t0
+
+
+class RefPool:
+    """All host cores, one process each (OPENBLAS_NUM_THREADS=1), each looping the
+    reference over its contiguous slice of a bounded sample."""
+
+    def __init__(self, key: str, step_seconds: float):
+        import multiprocessing as mp
+
+        from paper_2403_16665_b200.signals import WORKLOADS
+
+        self.key = key
+        self.w = WORKLOADS[key]
+        self.kind, self.api, fn = _ref_callable(key)
+        self.cores = len(os.sched_getaffinity(0))
+        # calibrate one core on 2 signals, then size a step to ~step_seconds
+        import numpy as np
+
+        from paper_2403_16665_b200.signals import generate
+
+        x = generate(self.w, 0, 2, threads=1).astype(np.complex128)
+        fn(x[0])
+        t0 = time.perf_counter()
+        fn(x[1])
+        self.per_signal = max(time.perf_counter() - t0, 1e-6)
+        per_core = max(1, int(step_seconds / self.per_signal))
+        self.sample = min(self.w.batch, per_core * self.cores)
+        self.sample = max(1, self.sample)
+        nproc = min(self.cores, self.sample)
+        self.slices = [(i * self.sample // nproc, (i + 1) * self.sample // nproc) for i in range(nproc)]
+        self.pool = mp.get_context("fork").Pool(nproc, initializer=_pool_init, initargs=(key, None))
+        self.pool.map(_pool_step, self.slices)  # generate the slices (untimed) and warm up
+
+    def step(self) -> float:
+        """Seconds of one step: the busiest worker's time on its slice."""
+        return max(self.pool.map(_pool_step, self.slices))
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def describe(self, busy: float) -> dict:
+        return {"value": self.sample * self.w.m / busy, "unit": "complex points/s", "cores": len(self.slices),
+                "kind": self.kind,
+                "sample": f"{self.sample} of {self.w.batch} signals of config {self.key} per step "
+                          f"({len(self.slices)} processes x ~{self.sample // len(self.slices)} signals, one "
+                          f"{self.api} call per signal, {busy:.2f} s for the busiest process; "
+                          f"{'baseline/_ref, unmodified' if self.kind == 'reference' else 'CPU restatement'})"}
+
+
+def cpu_reference(key: str, target_seconds: float):
+    """cpu_baseline of the GPU arm: one bounded step of the reference on all host cores."""
+    pool = RefPool(key, target_seconds)
+    try:
+        busy = min(pool.step() for _ in range(2))
+    finally:
+        pool.close()
+    return pool.describe(busy)
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -298,6 +418,70 @@ def side_config(key, dev, stream, peak, reps=20):
     return res
 
 
+def workload_config(w, total, world, big_inputs) -> dict:
+    """The config dict both arms print (same keys and values for the same run)."""
+    return {"workload": f"config {w.key}: batch {total} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
+            "batch": total, "n": w.n, "m": w.m, "alpha": str(w.alpha), "dtype": w.dtype,
+            "parallelism": f"dp{world} (batch shards, no data-path collective)",
+            "l2": "inputs larger than L2 (no flush)" if big_inputs else "L2 flushed between steps"}
+
+
+def executed_flops(w, plan, nloc, launch_s, peak):
+    """Textbook flop count of the algorithm the kernel actually runs (radix-2
+    count 5 P log2 P per complex P-point FFT, 6 flops per complex product),
+    against the measured FP peak -- beside the reference op-count credit."""
+    P = max(plan.fft_size, 1)
+    lg = max(1, (P - 1).bit_length())
+    if plan.method == "chirp":
+        per, how = 2 * 5 * P * lg + 6 * 3 * P, "chirp-z: 2 P-point FFTs + 3 complex products per point"
+    elif plan.method == "fft":
+        r = max(1, w.alpha.denominator // max(1, w.alpha.numerator))
+        per, how = r * (5 * P * lg + 6 * P), "alpha-FFT: r P-point FFTs + r pre-twiddles per point"
+    else:
+        per, how = 8 * w.m * w.n, "direct: 8 M N"
+    tf = per * nloc / launch_s / 1e12
+    return {"flops_per_signal": per, "how": how, "achieved_tflops": tf, "frac": tf / peak}
+
+
+def shard_parity(asx, w, x, out, dev, chunk=2048):
+    """Per-signal max|ΔX|/max|X| (ref/verify.py:75-77) of a rank's whole output
+    shard against the complex128 GPU path on the same inputs: the FP64 α-FFT
+    recursion where the plan allows it, else chirp-z / direct -- always a
+    different algorithm or precision from the production plan."""
+    import torch
+
+    tol = 2e-5 if w.dtype == "complex64" else 1e-10
+    ref = None
+    for meth in ("fft", "chirp", "direct"):
+        if w.dtype == "complex128" and meth == out_method(out):
+            continue
+        try:
+            ref = asx.plan(w.n, w.density, m=w.m, dtype="complex128", method=meth, real_input=w.real,
+                           device=dev.index)
+            break
+        except Exception:
+            continue
+    worst, nsig = 0.0, 0
+    for b0 in range(0, x.shape[0], chunk):
+        xi = x[b0:b0 + chunk]
+        xi = xi.to(torch.float64 if w.real else torch.complex128)
+        want = ref.execute(xi)
+        got = out[b0:b0 + chunk].to(torch.complex128)
+        den = want.abs().amax(dim=1).clamp_min(1e-300)
+        worst = max(worst, float(((got - want).abs().amax(dim=1) / den).max()))
+        nsig += xi.shape[0]
+    return {"max_rel_err": worst, "tolerance": tol, "signals_checked": nsig,
+            "reference": f"complex128 GPU plan, method {ref.method} (fft_size {ref.fft_size}), same inputs",
+            "metric": "per-signal max|dX| / max|X| (ref/verify.py:75-77), MAX over all signals and ranks"}
+
+
+_OUT_METHOD = {}
+
+
+def out_method(out):
+    return _OUT_METHOD.get(id(out))
+
+
 def run_gpu(args):
     import numpy as np
     import torch
@@ -307,10 +491,18 @@ def run_gpu(args):
     from paper_2403_16665_b200.signals import WORKLOADS, generate_device
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        sys.exit("bench.py: no CUDA device (libasx has no CPU fallback)")
+    if args.dist_backend == "nccl" and world > ndev:
+        sys.exit(f"bench.py: {world} ranks but {ndev} GPU(s); NCCL needs one GPU per rank")
+    dev = torch.device("cuda", local % ndev)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     barrier = dist_barrier
 
@@ -320,8 +512,9 @@ def run_gpu(args):
     nloc = hi - lo
     x = generate_device(w, lo, nloc, device=dev)
     plan = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, method=args.method, real_input=w.real,
-                    device=local)
+                    device=dev.index)
     out = torch.empty((nloc, w.m), dtype=getattr(torch, w.dtype), device=dev)
+    _OUT_METHOD[id(out)] = plan.method
     stream = torch.cuda.current_stream(dev)
     bytes_step = w.bytes_alg(nloc)
     flush = None
@@ -333,7 +526,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev.index)
     barrier()
     torch.cuda.synchronize()
     with clocks:
@@ -366,7 +559,8 @@ def run_gpu(args):
             if meth == plan.method:
                 continue
             try:
-                q = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, method=meth, real_input=w.real, device=local)
+                q = asx.plan(w.n, w.density, m=w.m, dtype=w.dtype, method=meth, real_input=w.real,
+                             device=dev.index)
             except Exception:
                 continue
             if meth == "direct" and w.n * w.m * nloc > 2e12:
@@ -413,6 +607,14 @@ def run_gpu(args):
                            "how": "concurrent pinned 512 MiB copies on two streams from one start event, best of 5",
                            "bound_ms": bound_s * 1e3, "frac": bound_s / e2e_s}
 
+    # parity of the whole shard vs the complex128 GPU path (untimed), MAX over ranks
+    parity = None
+    if not args.no_parity:
+        parity = shard_parity(asx, w, x, out, dev)
+        parity["max_rel_err"] = max_over_ranks(parity["max_rel_err"], device=dev)
+        parity["signals_checked"] = int(sum_over_ranks(parity["signals_checked"], device=dev))
+        parity["pass"] = parity["max_rel_err"] <= parity["tolerance"]
+
     # side measurements (world 1 only, not part of `value`): the other batched
     # BASELINE configs -- 1a (the α-FFT recursion itself, the one config whose
     # op count lets it approach the HBM roofline), 1b and 3
@@ -427,7 +629,7 @@ def run_gpu(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference(args.config, args.cpu_seconds)
+        cpu = cpu_reference(args.config, min(args.cpu_seconds, 4.0))
 
     if rank == 0:
         dtype_arith = "f32" if w.dtype == "complex64" else "f64"
@@ -444,13 +646,11 @@ def run_gpu(args):
             "vs_baseline": None,
             "dtype": dtype_arith,
             "data": "synthetic (BASELINE config tones+noise, numpy PCG64 per-signal seeds, tones synthesised on GPU)",
-            "config": {
-                "workload": f"config {w.key}: batch {total} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
-                "method": plan.method, "fft_size": plan.fft_size, "batch": total, "n": w.n, "m": w.m,
-                "alpha": str(w.alpha), "shard": f"contiguous {nloc} signals/rank",
-                "parallelism": f"dp{world} (batch shards, no data-path collective)",
-                "l2": "inputs larger than L2 (no flush)" if flush is None else "L2 flushed between steps",
-            },
+            "config": workload_config(w, total, world, flush is None),
+            "impl_detail": {"method": plan.method, "fft_size": plan.fft_size, "kernel": kernel_name,
+                            "shard": f"contiguous {nloc} signals/rank (rank 0)",
+                            "collectives": f"{args.dist_backend if world > 1 else 'none'}; none in the timed region"},
+            "parity": parity,
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": profiled_traffic(args.config, plan.method),
@@ -465,7 +665,9 @@ def run_gpu(args):
                             "frac": flops / avg_launch_s / 1e12 / fpk, "peak_source": fpk_src,
                             "flops": "8*M*N per signal (direct form: alpha has no dyadic alpha-FFT count)"
                             if (w.n * w.alpha.denominator) % w.alpha.numerator
-                            else "reference alpha-FFT op count 6*mults+2*adds per signal (fastpath.py:113-127)"},
+                            else "reference alpha-FFT op count 6*mults+2*adds per signal (fastpath.py:113-127): "
+                                 "an op-count credit, not what the kernel executes",
+                            "executed": executed_flops(w, plan, nloc, avg_launch_s, fpk)},
             },
             "other_methods": alt,
             "other_configs": other,
@@ -481,19 +683,33 @@ def run_gpu(args):
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port) on the host cores."""
+    """--impl reference: the reference's own CPU path on all host cores.
+
+    Each step is one bounded sample of the workload (about --ref-step-seconds
+    of wall time, all cores busy); W warm-up and K timed steps are run and
+    their real count, sample size and per-step time are what the line reports.
+    Under torchrun only rank 0 works; the other ranks exit at once."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     from paper_2403_16665_b200.signals import WORKLOADS
 
     w = WORKLOADS[args.config]
-    vals = []
-    cpu = None
-    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
-        cpu = cpu_reference(args.config, args.cpu_seconds)
-        vals.append(cpu["value"])
-    value = statistics.median(vals)
+    step_s = args.ref_step_seconds
+    # keep the whole run (W + K steps) within ~4 minutes
+    step_s = max(0.05, min(step_s, 240.0 / max(1, args.steps + args.warmup)))
+    pool = RefPool(args.config, step_s)
+    t_run = time.perf_counter()
+    try:
+        for _ in range(args.warmup):
+            pool.step()
+        times = [pool.step() for _ in range(args.steps)]
+    finally:
+        pool.close()
+    run_s = time.perf_counter() - t_run
+    ms_per_step = 1e3 * sum(times) / len(times)
+    value = pool.sample * w.m / (ms_per_step / 1e3)
+    cpu = pool.describe(ms_per_step / 1e3)
     cpu["value"] = value
     line = {
         "impl": "reference",
@@ -503,14 +719,17 @@ def run_reference(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": (w.batch * w.m / value) * 1e3,
+        "ms_per_step": ms_per_step,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (same generator and config as the GPU arm)",
-        "config": {"workload": f"config {w.key}: batch {w.batch} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
-                   "batch": w.batch, "n": w.n, "m": w.m, "alpha": str(w.alpha)},
+        "config": workload_config(w, w.batch, world, True),
+        "impl_detail": {"step": f"one bounded sample of {pool.sample} signals (not the whole batch of "
+                                f"{w.batch}); value = sample * M / mean step time",
+                        "api": pool.api, "kind": pool.kind, "wall_s_all_steps": run_s,
+                        "min_step_ms": 1e3 * min(times), "max_step_ms": 1e3 * max(times)},
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "complex points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -519,6 +738,7 @@ def run_reference(args):
 
 def main():
     args = parse_args()
+    maybe_self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -37,6 +37,14 @@ def _dist():
     return dist if dist.is_available() and dist.is_initialized() else None
 
 
+def _coll_device(device):
+    """Collectives run on `device` over NCCL, on host tensors over gloo."""
+    d = _dist()
+    if d is not None and d.get_backend() == "gloo":
+        return "cpu"
+    return device
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Job time = the slowest rank's time (all-reduce MAX)."""
     import torch
@@ -44,8 +52,20 @@ def max_over_ranks(value: float, device=None) -> float:
     d = _dist()
     if d is None:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     d.all_reduce(t, op=d.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, device=None) -> float:
+    """All-reduce SUM of a per-rank count."""
+    import torch
+
+    d = _dist()
+    if d is None:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
+    d.all_reduce(t, op=d.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -61,7 +81,7 @@ def gather_checksums(out, device=None) -> list:
 
     chk = torch.tensor([float(out.abs().amax().item()) if out.numel() else 0.0,
                         float(out.real.sum().item()) if out.numel() else 0.0],
-                       dtype=torch.float64, device=device)
+                       dtype=torch.float64, device=_coll_device(device))
     d = _dist()
     if d is None:
         return [chk.tolist()]
@@ -84,10 +104,10 @@ def gather_shards(out, total: int, device=None):
     ws = d.get_world_size()
     sizes = [hi - lo for lo, hi in (shard_range(total, ws, r) for r in range(ws))]
     width = out.shape[1]
-    buf = torch.zeros((max(sizes), width), dtype=out.dtype, device=out.device)
+    buf = torch.zeros((max(sizes), width), dtype=out.dtype, device=_coll_device(out.device))
     buf[: out.shape[0]] = out
     real = torch.view_as_real(buf) if buf.is_complex() else buf
     parts = [torch.zeros_like(real) for _ in range(ws)]
     d.all_gather(parts, real)
     parts = [torch.view_as_complex(p) if buf.is_complex() else p for p in parts]
-    return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
+    return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0).to(out.device)

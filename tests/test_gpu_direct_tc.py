@@ -148,13 +148,16 @@ def test_scale_at_the_edges_of_the_float_range(asx):
             assert orc.rel_err(got[i:i + 1], want[i:i + 1]) <= TOL, (i, amp[i])
         else:
             scale = np.max(np.abs(want[i]))
-            assert np.max(np.abs(got[i] - want[i])) <= max(TOL * scale, 1e-44 * n), (i, amp[i])
+            assert np.max(np.abs(got[i] - want[i])) <= max(TOL * scale, 2.0 ** -148), (i, amp[i])
 
 
-@pytest.mark.parametrize("n", [2048, 4096])
+@pytest.mark.parametrize("n", [512, 1024])
 def test_long_signals_at_the_cap(asx, n):
-    """The longest K the tensor-core form takes (N <= 4096; longer plans use
-    chirp-z): tone signals, fp32 TMEM accumulation over 4096 terms."""
+    """The longest K the tensor-core form takes (N <= 1024; longer plans use
+    chirp-z): coherent tone signals inside the window, where every partial sum
+    is as large as the result, so the tensor core's non-round-to-nearest fp32
+    accumulation (6 N / 16 steps per output) is at its worst.  Measured 2.6e-5
+    at N = 2048, hence the cap."""
     a, d, m = 1, 16, 256
     t = np.arange(n)
     rng = np.random.default_rng(n)
@@ -166,5 +169,6 @@ def test_long_signals_at_the_cap(asx, n):
     got = _run(asx, x, n, a, d, m)
     assert _variant() == VARIANT_DTC
     assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
-    p = asx.plan(8192, asx.DenseFactor(d, a), m=m, dtype="complex64", method="auto")
-    assert p.method != "direct" or n <= 4096
+    # past the cap `auto` takes chirp-z
+    p = asx.plan(2048, asx.DenseFactor(d, a), m=m, dtype="complex64", method="auto")
+    assert p.method == "chirp"
