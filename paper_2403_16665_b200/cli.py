@@ -2,7 +2,10 @@
 
 Mirrors the reference's ``alpha-spectra`` front end (ref/cli.py:1-13) for the
 transform path: ``compute`` (file -> spectrum file), ``verify`` (the
-cross-checking suites), ``bench`` (device-time grid over N x alpha x method).
+cross-checking suites), ``bench`` (the reference's count / time grid with its
+scaling-claim verdicts, JSON + CSV in the reference schema, device-timed on
+GPU plans: gridbench.py) and ``bench-device`` (batched device-time grid over
+N x alpha x method).
 Exit codes are the reference's: 0 ok, 1 verification failure, 2 parse error,
 3 alpha incompatible with N, 4 size unsupported by the method, 5 claim failure.
 ``--method auto`` never falls back to a CPU path: it picks among the GPU
@@ -15,7 +18,7 @@ import argparse
 import json
 import sys
 
-from . import fileio, verify
+from . import fileio, gridbench, verify
 from .core import DenseFactor, IncompatibleAlphaError, Signal, Spectrum, UnsupportedSizeError
 
 EXIT_OK, EXIT_VERIFY_FAILED, EXIT_PARSE_ERROR, EXIT_BAD_ALPHA, EXIT_BAD_SIZE, EXIT_CLAIM_FAILED = 0, 1, 2, 3, 4, 5
@@ -45,6 +48,14 @@ def _alphas(text):
         raise argparse.ArgumentTypeError(str(exc)) from None
 
 
+def _grid_methods(text):
+    names = [v.strip() for v in text.split(",") if v.strip()]
+    bad = [v for v in names if v not in gridbench.METHODS]
+    if bad:
+        raise argparse.ArgumentTypeError(f"unknown method {bad[0]!r} (choose from {', '.join(gridbench.METHODS)})")
+    return names
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="paper_2403_16665_b200",
                                  description="GPU α-DFT / α-FFT: spectra with bin density alpha = p/q.")
@@ -60,7 +71,17 @@ def build_parser() -> argparse.ArgumentParser:
     v.add_argument("--seed", type=int, default=0)
     v.add_argument("--sizes", type=_ints, default=list(verify.DEFAULT_SIZES))
     v.add_argument("--inject-fault", action="store_true", help=argparse.SUPPRESS)
-    b = sub.add_parser("bench", help="device-time grid over N x alpha x method")
+    g = sub.add_parser("bench", help="run the benchmark grid and judge the scaling claims (reference schema)")
+    g.add_argument("--grid-n", type=_ints, default=[64, 128, 256, 512, 1024])
+    g.add_argument("--grid-alpha", type=_alphas,
+                   default=[DenseFactor(1, 8), DenseFactor(1, 4), DenseFactor(1, 2), DenseFactor(1), DenseFactor(2),
+                            DenseFactor(4), DenseFactor(8)])
+    g.add_argument("--methods", type=_grid_methods, default=["alpha_fft", "zeropad_fft"])
+    g.add_argument("--reps", type=int, default=20)
+    g.add_argument("--seed", type=int, default=0)
+    g.add_argument("--output", default=None, help="JSON report path")
+    g.add_argument("--csv", default=None, help="records CSV path")
+    b = sub.add_parser("bench-device", help="batched device-time grid over N x alpha x method")
     b.add_argument("--grid-n", type=_ints, default=[256, 1024, 4096])
     b.add_argument("--grid-alpha", type=_alphas, default=[DenseFactor(1), DenseFactor(2), DenseFactor(8)])
     b.add_argument("--methods", default="fft,chirp,direct")
@@ -119,6 +140,33 @@ def cmd_verify(args) -> int:
 
 
 def cmd_bench(args) -> int:
+    """The reference's `bench` (ref/cli.py:188-216) on GPU plans: exit 0 when
+    every claim passes, 5 when one fails, 2 for an empty grid."""
+    skipped = []
+    records = gridbench.run_grid(args.grid_n, args.grid_alpha, args.methods, reps=args.reps, seed=args.seed,
+                                 skipped=skipped)
+    if not records:
+        print("error: no runnable grid cells", file=sys.stderr)
+        return EXIT_PARSE_ERROR
+    report = gridbench.make_report(records, skipped)
+    if args.output:
+        report.write_json(args.output)
+        print(f"wrote {args.output} ({len(records)} records)")
+    if args.csv:
+        report.write_csv(args.csv)
+        print(f"wrote {args.csv}")
+    for cell in skipped:
+        print(f"skipped N={cell['N']} alpha={cell['alpha_p']}/{cell['alpha_q']} {cell['method']}: {cell['reason']}")
+    for v in report.verdicts:
+        print(f"claim {v.claim}: {'pass' if v.passed else 'FAIL'}")
+        for w in v.warnings:
+            print(f"  warning: {w}")
+    if not report.verdicts:
+        print("warning: grid too small to evaluate any scaling claim")
+    return EXIT_OK if report.all_passed else EXIT_CLAIM_FAILED
+
+
+def cmd_bench_device(args) -> int:
     import torch
 
     from . import transforms
@@ -162,7 +210,8 @@ def cmd_bench(args) -> int:
 
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
-    return {"compute": cmd_compute, "verify": cmd_verify, "bench": cmd_bench}[args.command](args)
+    return {"compute": cmd_compute, "verify": cmd_verify, "bench": cmd_bench,
+            "bench-device": cmd_bench_device}[args.command](args)
 
 
 def entry() -> None:
