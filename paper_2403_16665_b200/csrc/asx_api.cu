@@ -93,6 +93,7 @@ struct asx_plan_s {
   int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
   // large chirp path (P > one CTA): four-step P = P1 x P2 through workspace A
   int large = 0;
+  int large_fft = 0;  // the α-FFT through the same four-step kernels (P = N > one CTA), one residue per launch pair
   int64_t P1 = 0, P2 = 0;
   int lfBig = 0;
   int row_local = 0;  // complex128 P2 = 8192: rows on k_large_rows_local, Ht stored permuted
@@ -299,7 +300,22 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
     lp.P2 = p->P2;
     const int dbl = p->dtype == ASX_C128;
     const size_t ie = in_elem(p), oe = celem(p->dtype);
-    for (int64_t b = 0; b < batch && e == cudaSuccess; ++b) {
+    if (p->large_fft) {
+      // α-FFT: one (columns, rows) launch pair per output residue c < min(r, M)
+      lp.P = p->n;
+      lp.r = p->r;
+      const int64_t nres = std::min<int64_t>(p->r, p->m);
+      for (int64_t b = 0; b < batch && e == cudaSuccess; ++b) {
+        lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
+        lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
+        for (int64_t c = 0; c < nres && e == cudaSuccess; ++c) {
+          lp.c = c;
+          e = launch_large(dbl, p->P1, COL_AFFT, 0, 0, lp, st);
+          if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_AFFT, 1, lp, st);
+        }
+      }
+    }
+    for (int64_t b = 0; b < batch && e == cudaSuccess && !p->large_fft; ++b) {
       lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
       lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
       e = launch_large(dbl, p->P1, COL_FWD_SIGNAL, 0, 0, lp, st);
@@ -389,10 +405,17 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   // (config 4: 2.6e-5 against 2e-5), so the inner size is
   // capped at the FP64 engine's maxP for both dtypes.
   const int maxP_fft = kMaxP_c128;
-  bool fft_ok = false;
+  bool fft_ok = false, fft_large = false;
   int64_t fft_r = 1, fft_fold = 1, fft_P = 0;
   if (a == 1 && is_pow2(n) && n <= maxP_fft) {
     fft_ok = true;
+    fft_r = d;
+    fft_P = n;
+  } else if (a == 1 && is_pow2(n) && is_pow2(d) && n > maxP_fft && n / maxP_fft <= 1024 && dtype == ASX_C128 &&
+             m <= d * n) {
+    // past one CTA: the four-step α-FFT (asx_large.cuh), complex128, power-of-two
+    // r as the reference's plan() requires (fastpath.py:97-101), bins m < r N
+    fft_ok = fft_large = true;
     fft_r = d;
     fft_P = n;
   } else if (d == 1 && n % a == 0 && is_pow2(n / a) && (n / a) <= maxP_fft) {
@@ -505,6 +528,12 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     p->r = fft_r;
     p->fold = fft_fold;
   }
+  int64_t twP1_sz = 0, twBig_sz = 0, A_sz = 0;
+  if (chosen == ASX_FFT && fft_large) {
+    p->large = p->large_fft = 1;
+    p->P2 = maxP_fft;
+    p->P1 = n / maxP_fft;
+  }
   // must equal TwSplit<P>::LF (asx_engine.cuh)
   auto lf_of_P = [](int P) {
     const int LP = log2i(P);
@@ -514,7 +543,14 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     if (chosen == ASX_CHIRP) p->P = (int)chirp_P;
     twP_sz = two_level_size(p->P, lf_of_P(p->P));
   }
-  if (chosen == ASX_FFT && p->r > 1) {
+  if (p->large_fft) {
+    twP_sz = two_level_size(p->P2, lf_of_P((int)p->P2));  // row FFT table W_P2
+    twP1_sz = two_level_size(p->P1, lf_of_P((int)p->P1));
+    p->lfBig = two_level_lf(p->r * n);
+    twBig_sz = two_level_size(p->r * n, p->lfBig);  // W_{rN}: α pre-twiddle and four-step twiddle
+    A_sz = n;
+  }
+  if (chosen == ASX_FFT && p->r > 1 && !p->large_fft) {
     p->lfA = two_level_lf(p->r * p->P);
     twA_sz = two_level_size(p->r * p->P, p->lfA);
   }
@@ -522,7 +558,6 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     chirp_sz = std::max(n, m);
     H_sz = p->P;
   }
-  int64_t twP1_sz = 0, twBig_sz = 0, A_sz = 0;
   if (chosen == ASX_CHIRP && chirp_large) {
     p->large = 1;
     p->P2 = maxP;
@@ -578,7 +613,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   char* base = static_cast<char*>(p->tables);
   if (twP_sz) fill_two_level(base + p->off_twP, p->large ? p->P2 : p->P, lf_of_P(p->large ? (int)p->P2 : p->P), dbl, st);
   if (twP1_sz) fill_two_level(base + p->off_twP1, p->P1, lf_of_P((int)p->P1), dbl, st);
-  if (twBig_sz) fill_two_level(base + p->off_twBig, chirp_P, p->lfBig, dbl, st);
+  if (twBig_sz) fill_two_level(base + p->off_twBig, p->large_fft ? p->r * n : chirp_P, p->lfBig, dbl, st);
   if (twA_sz) fill_two_level(base + p->off_twA, p->r * p->P, p->lfA, dbl, st);
   if (afl_sz) k_afl_image<<<(unsigned)((afl_sz + 255) / 256), 256, 0, st>>>(reinterpret_cast<double2*>(base + p->off_afl));
   double2* wP_d = nullptr;
@@ -686,7 +721,7 @@ int asx_plan_query(asx_plan_t p, asx_plan_info* info) {
   info->predicted_mults = p->pred_mults;
   info->predicted_adds = p->pred_adds;
   info->workspace_bytes = (int64_t)p->table_bytes;
-  info->kernels_per_execute = p->large ? 3 : 1;
+  info->kernels_per_execute = p->large_fft ? (int32_t)(2 * std::min<int64_t>(p->r, p->m)) : p->large ? 3 : 1;
   info->device = p->device;
   return ASX_OK;
 }

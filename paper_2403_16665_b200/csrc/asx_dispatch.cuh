@@ -359,7 +359,9 @@ cudaError_t launch_cols(int mode, const LParams& lp, cudaStream_t st) {
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, int64_t(sms) * std::max(per_sm, 1));
     if (e == cudaSuccess) kern<<<grid, G::NT * kColTile, G::SMEM, st>>>(lp);
   };
-  if (mode == COL_FWD_SIGNAL)
+  if (mode == COL_AFFT)
+    go(k_large_cols<Real, P1, G::NT, COL_AFFT>);
+  else if (mode == COL_FWD_SIGNAL)
     go(k_large_cols<Real, P1, G::NT, COL_FWD_SIGNAL>);
   else if (mode == COL_FWD_TABLE)
     go(k_large_cols<Real, P1, G::NT, COL_FWD_TABLE>);
@@ -418,7 +420,9 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
       return cudaGetLastError();
     }
   }
-  if (mode == ROW_SPECTRUM)
+  if (mode == ROW_AFFT)
+    go(k_large_rows<Real, P2, G::NT, ROW_AFFT>);
+  else if (mode == ROW_SPECTRUM)
     go(k_large_rows<Real, P2, G::NT, ROW_SPECTRUM>);
   else
     go(k_large_rows<Real, P2, G::NT, ROW_MAIN>);

@@ -14,6 +14,18 @@
 //   KC  k_large_cols<INV>: per tile of 8 columns c, FFT_P1 over k1 of
 //       B[k1][c] -> G[c + P2 d]; X[m] = chirp[m] * conj(G[m]) for m < M.
 // The plan builds Ht with KA (on h) + k_large_rows<SPECTRUM>.
+//
+// The same two kernels run the α-FFT itself (method fft) at sizes past one
+// CTA, α = 1/r with r a power of two (the reference's plan() rule,
+// fastpath.py:97-101), N = P1 x P2, one output residue c < r per launch pair:
+// bins m = c + r d, d = d1 + P1 d2, n = P2 n1 + n2,
+//   X[c + r d] = Σ_{n2} W_{P2}^{d2 n2} · W_{rN}^{(c + r d1) n2}
+//                · Σ_{n1} W_{P1}^{d1 n1} · W_{rP1}^{c n1} · x[P2 n1 + n2]
+//   KA  k_large_cols<AFFT>: per column n2, × W_{rP1}^{c n1} (the α pre-twiddle's
+//       n1 part), FFT_P1 over n1, × W_{rN}^{(c + r d1) n2} -> A[d1][n2]
+//   KB  k_large_rows<AFFT>: per row d1, FFT_P2 over n2 -> X[c + r(d1 + P1 d2)]
+//       for the d2 with m < M (the recursion's even/odd split per residue,
+//       DESIGN.md §2; twiddles exact: one two-level lookup of W_{rN}).
 #pragma once
 
 #include "asx_kernels.cuh"
@@ -50,6 +62,7 @@ struct LParams {
   double scale;         // plan time: 1/P
   int64_t P;            // P1 * P2
   int64_t P2;           // row length (row stride of A / Ht)
+  int64_t r, c;         // α-FFT modes: density r (power of two), residue c; twBig = W_{rN}
 };
 
 template <typename C>
@@ -59,7 +72,7 @@ __device__ __forceinline__ C tw_big(const C* tw, uint64_t k, int lf) {
   return cmul(f, c);
 }
 
-enum { COL_FWD_SIGNAL = 0, COL_FWD_TABLE = 1, COL_INV_OUT = 2 };
+enum { COL_FWD_SIGNAL = 0, COL_FWD_TABLE = 1, COL_INV_OUT = 2, COL_AFFT = 3 };
 
 template <typename Real, int P1>
 struct ColCfg {
@@ -79,7 +92,8 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   constexpr int R = E::R;
   constexpr int THREADS = NT * kColTile;
   const int64_t P2 = p.P2;
-  const uint64_t Pmask = uint64_t(p.P - 1);
+  // twBig period: P (chirp), r N (α-FFT; both powers of two)
+  const uint64_t Pmask = MODE == COL_AFFT ? uint64_t(p.r * p.P - 1) : uint64_t(p.P - 1);
   constexpr int CS = E::SMEM_ELEMS > P1 + (P1 >> E::LPAD) ? E::SMEM_ELEMS : P1 + (P1 >> E::LPAD);  // per-column stride
   extern __shared__ __align__(128) unsigned char smraw[];
   C* smbase = reinterpret_cast<C*>(smraw);
@@ -111,6 +125,13 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
           }
         } else if constexpr (MODE == COL_FWD_TABLE) {
           val = __ldg(reinterpret_cast<const C*>(p.h) + idx);
+        } else if constexpr (MODE == COL_AFFT) {
+          // x[P2 n1 + n2] × W_{rP1}^{c n1} = W_{rN}^{c n1 P2}
+          const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(p.x) + idx), Real(0))
+                                 : __ldg(reinterpret_cast<const C*>(p.x) + idx);
+          val = p.c ? cmul(xv, tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(p.c) * uint64_t(row) *
+                                                                          uint64_t(P2)) & Pmask, p.lfBig))
+                    : xv;
         } else {
           val = __ldg(reinterpret_cast<const C*>(p.A) + idx);  // B[k1][c], row = k1
         }
@@ -124,7 +145,15 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
     __syncthreads();       // tile reads done before the transform reuses sm
     E::run(v, sm, t, tr, xs);
     const int col = col0 + team;
-    if constexpr (MODE != COL_INV_OUT) {
+    if constexpr (MODE == COL_AFFT) {
+      // twiddle W_{rN}^{(c + r d1) n2}, d1 = t + NT*i
+  #pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint64_t e = (uint64_t(p.c) + uint64_t(p.r) * uint64_t(t + NT * i)) * uint64_t(col);
+        v[i] = cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), e & Pmask, p.lfBig));
+        if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+      }
+    } else if constexpr (MODE != COL_INV_OUT) {
       // twiddle W_P^{n2 k1}, k1 = t + NT*i
   #pragma unroll
       for (int i = 0; i < R; ++i) {
@@ -153,7 +182,7 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   }
 }
 
-enum { ROW_SPECTRUM = 0, ROW_MAIN = 1, ROW_MAIN_LOCAL = 2 };  // 2: k_large_rows_local (asx_chirp_local128.cuh)
+enum { ROW_SPECTRUM = 0, ROW_MAIN = 1, ROW_MAIN_LOCAL = 2, ROW_AFFT = 3 };  // 2: k_large_rows_local (asx_chirp_local128.cuh)
 
 __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -195,6 +224,16 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
       const Real s = Real(p.scale);
 #pragma unroll
       for (int i = 0; i < R; ++i) out[t + NT * i] = mk(v[i].x * s, v[i].y * s);
+    } else if constexpr (MODE == ROW_AFFT) {
+      // X[c + r (d1 + P1 d2)], d1 = k1, d2 = t + NT*i; bins past M are not stored
+      E::run(v, sm, t, tr, xs);
+      const int64_t P1 = p.P / P2;
+      C* X = reinterpret_cast<C*>(p.X);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int64_t mm = p.c + p.r * (int64_t(k1) + P1 * int64_t(t + NT * i));
+        if (mm < p.m) X[mm] = v[i];
+      }
     } else {
       const C* ht = reinterpret_cast<const C*>(p.Ht) + int64_t(k1) * P2;
       // one FFT body, two trips (forward step 3, then inverse step 1)

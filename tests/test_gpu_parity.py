@@ -318,14 +318,19 @@ def test_large_chirp_vs_oracle(asx, n, a, d, m, dtype):
     assert orc.rel_err(got, want) <= tol
 
 
-def test_config2_full_size(asx):
-    """BASELINE config 2: N = 2^22 real f64, alpha = 1/16, M = N (four-step chirp)."""
+@pytest.mark.parametrize("method", ["auto", "fft"])
+def test_config2_full_size(asx, method):
+    """BASELINE config 2: N = 2^22 real f64, alpha = 1/16, M = N: the four-step
+    chirp (auto) and the paper's α-FFT recursion past one CTA (fft: 16 residues,
+    each a four-step 2^22-point transform)."""
     from paper_2403_16665_b200.signals import WORKLOADS, generate
 
     w = WORKLOADS["2"]
     x = generate(w, 0, 1)[0]
-    got, p = gpu_run(asx, x[None], 1, 16, w.m, "auto", real=True)
-    assert p.method == "chirp"
+    got, p = gpu_run(asx, x[None], 1, 16, w.m, method, real=True)
+    assert p.method == ("chirp" if method == "auto" else "fft")
+    if method == "fft":
+        assert p.info.kernels_per_execute == 32
     # independent check: zero-padded FFT (pocketfft) of length 16N, first N bins
     want = np.fft.fft(x, 16 * w.n)[: w.m]
     assert orc.rel_err(got, want[None]) <= TOL64
@@ -337,6 +342,33 @@ def test_config2_full_size(asx):
         idx = (b * nn) % L
         want_b = np.sum(x * np.exp(-2j * np.pi * idx / L))
         assert abs(got[0, b] - want_b) <= TOL64 * np.max(np.abs(got))
+
+
+@pytest.mark.parametrize("n,d,m,real", [
+    (16384, 2, 16384, False),        # P1 = 2
+    (32768, 4, 20000, True),         # ragged M, real input
+    (1 << 17, 8, 1 << 20, False),    # every bin of the density-8 spectrum (M = r N)
+])
+def test_large_alpha_fft_vs_oracle(asx, n, d, m, real):
+    """The α-FFT past one CTA (four-step, one residue per launch pair) against
+    the zero-padded FFT (first M bins of the density-d spectrum) and the oracle's
+    exact-reduction sums on sampled bins."""
+    rng = np.random.default_rng(n + d)
+    x = rng.standard_normal((2, n)) if real else np.stack([orc.unit_disk(rng, n) for _ in range(2)])
+    got, p = gpu_run(asx, x, 1, d, m, "fft", real=real)
+    assert p.method == "fft" and p.info.kernels_per_execute == 2 * d
+    want = np.fft.fft(x.astype(np.complex128), d * n, axis=1)[:, :m]
+    assert orc.rel_err(got, want) <= TOL64
+    # exact-reduction direct sums on sampled bins (ref/oracle.py:37-47 semantics)
+    nn = np.arange(n, dtype=np.int64)
+    for b in (0, 1, 5, m // 3, m - 1):
+        want_b = (x * np.exp(-2j * np.pi * ((b * nn) % (d * n)) / (d * n))).sum(axis=1)
+        assert np.max(np.abs(got[:, b] - want_b)) <= TOL64 * np.max(np.abs(got))
+    # the reference's plan() rule past one CTA: power-of-two density only
+    with pytest.raises(asx.UnsupportedSizeError):
+        asx.plan(16384, asx.DenseFactor(3), m=16384, method="fft")
+    with pytest.raises(asx.UnsupportedSizeError):
+        asx.plan(16384, asx.DenseFactor(2), m=16384, dtype="complex64", method="fft")
 
 
 def test_lazy_conjugate_views_are_resolved(asx, torch):
