@@ -18,6 +18,7 @@
 
 #include "../../include/asx.h"
 #include "asx_direct_tc.cuh"
+#include "asx_direct_tc2.cuh"
 #include "asx_dispatch.cuh"
 
 using namespace asx;
@@ -87,7 +88,7 @@ struct asx_plan_s {
   size_t table_bytes = 0;
   size_t off_twP = 0, off_twA = 0, off_chirp = 0, off_H = 0, off_W = 0;
   size_t off_afl = 0;
-  int dtc = 0;            // direct form on the tensor cores (k_direct_tc, complex64)
+  int dtc = 0;            // direct form on the tensor cores: 1 k_direct_tc (M = 128), 2 k_direct_tc2 (M = 256, CTA pairs)
   size_t off_vimg = 0;    // its fp16 operand image (bytes from tables)
   int lfA = 0;
   int tw_elems = 0;  // shared-memory twiddle elements (twP [+ twA])
@@ -237,6 +238,24 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
       k_direct_small<float><<<grid, 256, 0, st>>>(kp);
     else
       k_direct_small<double><<<grid, 256, 0, st>>>(kp);
+    e = cudaGetLastError();
+  } else if (p->method == ASX_DIRECT && p->dtc == 2 && dtc_aligned(x, xs, X, Xs) && p->env.sms >= 2) {
+    dtc2::Params dp;
+    dp.x = static_cast<const float*>(x);
+    dp.xs = xs;
+    dp.X = static_cast<float*>(X);
+    dp.Xs = Xs;
+    dp.batch = batch;
+    dp.n = (int)p->n;
+    dp.wimg = static_cast<const unsigned char*>(p->tables) + p->off_vimg;
+    const int64_t tiles = (batch + dtc2::TS - 1) / dtc2::TS;
+    const int grid = 2 * (int)std::min<int64_t>(tiles, p->env.sms / 2);
+    dtc2::k_direct_tc2<<<grid, dtc2::NTHREADS, dtc2::SMEM_BYTES, st>>>(dp);
+    g_last_launch.grid = grid;
+    g_last_launch.block = dtc2::NTHREADS;
+    g_last_launch.smem = dtc2::SMEM_BYTES;
+    g_last_launch.staged = 1;
+    g_last_launch.tmem = 10;
     e = cudaGetLastError();
   } else if (p->method == ASX_DIRECT && p->dtc && dtc_aligned(x, xs, X, Xs)) {
     dtc::Params dp;
@@ -570,7 +589,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   }
   if (chosen == ASX_DIRECT) W_sz = m * n;
   if (chosen == ASX_DIRECT && dtc_ok) {
-    p->dtc = 1;
+    const char* no_pair = std::getenv("ASX_NO_DTC_PAIR");
+    p->dtc = (m == dtc2::MB && !(no_pair && no_pair[0] == '1')) ? 2 : 1;
     W_sz = 2 * m * n;  // complex W (small-batch / misaligned launches) + the fp16 Wr/Wi hi/lo image (8 m n bytes)
   }
   const bool afl = chosen == ASX_FFT && dtype == ASX_C128 && p->P == AfftLocal::P && p->r == 2 && p->fold == 1;
@@ -669,7 +689,12 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     const int64_t total = m * n;
     k_dft_matrix<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
         base + p->off_W, m, n, (uint64_t)a, L, dbl);
-    if (p->dtc) {
+    if (p->dtc == 2) {
+      dtc2::k_direct_tc2_image<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
+          reinterpret_cast<unsigned char*>(base + p->off_vimg), (int)n, (uint64_t)a, L);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(dtc2::k_direct_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, dtc2::SMEM_BYTES);
+    } else if (p->dtc) {
       dtc::k_direct_tc_image<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
           reinterpret_cast<unsigned char*>(base + p->off_vimg), (int)n, (int)m, (uint64_t)a, L);
       if (e == cudaSuccess)

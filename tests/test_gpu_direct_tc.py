@@ -18,6 +18,7 @@ from oracle import alpha_oracle as orc
 
 pytestmark = pytest.mark.gpu
 
+VARIANT_DTC_PAIR = 10  # asx_last_launch: k_direct_tc2 (M = 256, CTA pairs)
 VARIANT_DTC = 8  # asx_last_launch: k_direct_tc
 TOL = 2e-5
 
@@ -49,13 +50,13 @@ def _run(asx, x, n, a, d, m, method="direct"):
     return got
 
 
-@pytest.mark.parametrize("batch", [9, 127, 128, 129, 1000, 20000])
+@pytest.mark.parametrize("batch", [9, 63, 64, 65, 127, 128, 129, 255, 257, 1000, 20000, 40000])
 def test_config3_shape(asx, batch):
     n, a, d, m = 256, 37, 100, 256
     rng = np.random.default_rng(batch)
     x = np.stack([orc.unit_disk(rng, n) for _ in range(batch)]).astype(np.complex64)
     got = _run(asx, x, n, a, d, m)
-    assert _variant() == VARIANT_DTC
+    assert _variant() == VARIANT_DTC_PAIR  # M = 256: the CTA-pair kernel
     assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
 
 
@@ -65,8 +66,35 @@ def test_shapes(asx, n, a, d, m):
     rng = np.random.default_rng(n + m)
     x = np.stack([orc.unit_disk(rng, n) for _ in range(300)]).astype(np.complex64)
     got = _run(asx, x, n, a, d, m)
-    assert _variant() == VARIANT_DTC
+    assert _variant() in (VARIANT_DTC, VARIANT_DTC_PAIR)
     assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
+
+
+def test_pair_kernel_matches_single_cta_kernel(asx):
+    """k_direct_tc2 (CTA pairs, M = 256) against k_direct_tc on the same inputs:
+    the same fp16 hi/lo products, so agreement to a few fp32 ulps of max|X|."""
+    import os
+    import subprocess
+    import sys
+
+    n, a, d, m = 256, 37, 100, 256
+    rng = np.random.default_rng(17)
+    x = np.stack([orc.unit_disk(rng, n) for _ in range(3000)]).astype(np.complex64)
+    got = _run(asx, x, n, a, d, m)
+    assert _variant() == VARIANT_DTC_PAIR
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, %r); import paper_2403_16665_b200 as asx;"
+            "x = np.load(sys.argv[1]); p = asx.plan(256, asx.DenseFactor(100, 37), m=256, dtype='complex64', "
+            "method='direct'); np.save(sys.argv[2], p.execute(torch.from_numpy(x).cuda()).cpu().numpy())")
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        np.save(os.path.join(td, "x.npy"), x)
+        env = dict(os.environ, ASX_NO_DTC_PAIR="1")
+        repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        subprocess.run([sys.executable, "-c", code % repo, os.path.join(td, "x.npy"), os.path.join(td, "y.npy")],
+                       check=True, env=env)
+        single = np.load(os.path.join(td, "y.npy"))
+    assert orc.rel_err(got, single) <= 2e-6
 
 
 def test_alpha_one_is_fft(asx):
@@ -85,7 +113,7 @@ def test_per_signal_scaling(asx):
     amp = np.array([1e-6, 1e4, 1.0, 3e-3, 7e2, 1e-12, 1e12, 0.0] * 32)
     x = (x * amp[:, None]).astype(np.complex64)
     got = _run(asx, x, n, a, d, m)
-    assert _variant() == VARIANT_DTC
+    assert _variant() in (VARIANT_DTC, VARIANT_DTC_PAIR)
     want = orc.direct(x.astype(np.complex128), a, d, m)
     live = amp != 0.0
     assert orc.rel_err(got[live], want[live]) <= TOL
@@ -112,7 +140,7 @@ def test_strided_rows(asx, stride):
     p = asx.plan(n, asx.DenseFactor(d, a), m=m, dtype="complex64", method="direct")
     got = p.execute(torch.from_numpy(buf).cuda()[:, :n]).cpu().numpy()
     if stride % 2 == 0:
-        assert _variant() == VARIANT_DTC
+        assert _variant() in (VARIANT_DTC, VARIANT_DTC_PAIR)
     assert orc.rel_err(got, orc.direct(buf[:, :n].astype(np.complex128), a, d, m)) <= TOL
 
 
@@ -137,7 +165,7 @@ def test_scale_at_the_edges_of_the_float_range(asx):
     x = np.stack([orc.unit_disk(rng, n) for _ in range(amp.size)]) * amp[:, None]
     x = x.astype(np.complex64)
     got = _run(asx, x, n, a, d, m)
-    assert _variant() == VARIANT_DTC
+    assert _variant() in (VARIANT_DTC, VARIANT_DTC_PAIR)
     want = orc.direct(x.astype(np.complex128), a, d, m)
     assert np.all(np.isfinite(got))
     # |X| <= N max|x| stays finite in fp32 for these amplitudes; subnormal
@@ -167,7 +195,7 @@ def test_long_signals_at_the_cap(asx, n):
         rows.append(sum(np.exp(2j * np.pi * fk * t / n) for fk in f) + 0.01 * orc.unit_disk(rng, n))
     x = np.stack(rows).astype(np.complex64)
     got = _run(asx, x, n, a, d, m)
-    assert _variant() == VARIANT_DTC
+    assert _variant() in (VARIANT_DTC, VARIANT_DTC_PAIR)
     assert orc.rel_err(got, orc.direct(x.astype(np.complex128), a, d, m)) <= TOL
     # past the cap `auto` takes chirp-z
     p = asx.plan(2048, asx.DenseFactor(d, a), m=m, dtype="complex64", method="auto")

@@ -82,7 +82,7 @@ def test_guard_bands(env, case, pad):
         f"{label}: store outside the output rows"
     idx = np.unique(np.linspace(0, batch - 1, 5).astype(int))
     want = orc.direct(x[idx].astype(np.complex128), a, d, m)
-    assert orc.rel_err(o[1:batch + 1][idx], want) <= TOL[dtype], label
+    assert orc.rel_err(o[1:batch + 1, :m][idx], want) <= TOL[dtype], label
 
 
 @pytest.mark.parametrize("case", KERNELS, ids=[k[0] for k in KERNELS])
