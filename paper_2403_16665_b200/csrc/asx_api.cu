@@ -18,7 +18,12 @@
 
 #include "../../include/asx.h"
 #include "asx_direct_tc.cuh"
+#ifndef ASX_DTC_PAIR
+#define ASX_DTC_PAIR 0
+#endif
+#if ASX_DTC_PAIR
 #include "asx_direct_tc2.cuh"
+#endif
 #include "asx_dispatch.cuh"
 
 using namespace asx;
@@ -239,6 +244,7 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
     else
       k_direct_small<double><<<grid, 256, 0, st>>>(kp);
     e = cudaGetLastError();
+#if ASX_DTC_PAIR
   } else if (p->method == ASX_DIRECT && p->dtc == 2 && dtc_aligned(x, xs, X, Xs) && p->env.sms >= 2) {
     dtc2::Params dp;
     dp.x = static_cast<const float*>(x);
@@ -257,6 +263,7 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
     g_last_launch.staged = 1;
     g_last_launch.tmem = 10;
     e = cudaGetLastError();
+#endif
   } else if (p->method == ASX_DIRECT && p->dtc && dtc_aligned(x, xs, X, Xs)) {
     dtc::Params dp;
     dp.x = static_cast<const float*>(x);
@@ -589,8 +596,10 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
   }
   if (chosen == ASX_DIRECT) W_sz = m * n;
   if (chosen == ASX_DIRECT && dtc_ok) {
-    const char* no_pair = std::getenv("ASX_NO_DTC_PAIR");
-    p->dtc = (m == dtc2::MB && !(no_pair && no_pair[0] == '1')) ? 2 : 1;
+    // the CTA-pair kernel (k_direct_tc2) measured 0.39 ms on config 3 against
+    // 0.375 ms for k_direct_tc: built only in `make variant
+    // VFLAGS=-DASX_DTC_PAIR=1` for further tuning, not in the shipped library
+    p->dtc = (ASX_DTC_PAIR && m == 256) ? 2 : 1;
     W_sz = 2 * m * n;  // complex W (small-batch / misaligned launches) + the fp16 Wr/Wi hi/lo image (8 m n bytes)
   }
   const bool afl = chosen == ASX_FFT && dtype == ASX_C128 && p->P == AfftLocal::P && p->r == 2 && p->fold == 1;
@@ -689,12 +698,15 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     const int64_t total = m * n;
     k_dft_matrix<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
         base + p->off_W, m, n, (uint64_t)a, L, dbl);
+#if ASX_DTC_PAIR
     if (p->dtc == 2) {
       dtc2::k_direct_tc2_image<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
           reinterpret_cast<unsigned char*>(base + p->off_vimg), (int)n, (uint64_t)a, L);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(dtc2::k_direct_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, dtc2::SMEM_BYTES);
-    } else if (p->dtc) {
+    } else
+#endif
+    if (p->dtc) {
       dtc::k_direct_tc_image<<<(unsigned)std::min<int64_t>((total + 255) / 256, 65535), 256, 0, st>>>(
           reinterpret_cast<unsigned char*>(base + p->off_vimg), (int)n, (int)m, (uint64_t)a, L);
       if (e == cudaSuccess)

@@ -329,20 +329,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
               const uint32_t ko = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
               const uint64_t Bh = sdesc(bh + ko), Bl = sdesc(bl + ko);
               if (ASX_DTC_ABLATE & 1) {
-              } else if (part == 0) {  // Re += Ar Wr,  Im += Ai Wr
+              } else if (part == 0) {  // Re += Ar Wr,  Im += Ai Wr (alternating accumulators)
                 const uint32_t first = (c == 0 && k == 0) ? 0u : 1u;
                 mma_f16(d_re, sdesc(arh + ko), Bh, id, first);
-                mma_f16(d_re, sdesc(arh + ko), Bl, id, 1u);
-                mma_f16(d_re, sdesc(arl + ko), Bh, id, 1u);
                 mma_f16(d_im, sdesc(aih + ko), Bh, id, first);
+                mma_f16(d_re, sdesc(arh + ko), Bl, id, 1u);
                 mma_f16(d_im, sdesc(aih + ko), Bl, id, 1u);
+                mma_f16(d_re, sdesc(arl + ko), Bh, id, 1u);
                 mma_f16(d_im, sdesc(ail + ko), Bh, id, 1u);
               } else {  // Re -= Ai Wi,  Im += Ar Wi
                 mma_f16(d_re, sdesc(aih + ko), Bh, idn, 1u);
-                mma_f16(d_re, sdesc(aih + ko), Bl, idn, 1u);
-                mma_f16(d_re, sdesc(ail + ko), Bh, idn, 1u);
                 mma_f16(d_im, sdesc(arh + ko), Bh, id, 1u);
+                mma_f16(d_re, sdesc(aih + ko), Bl, idn, 1u);
                 mma_f16(d_im, sdesc(arh + ko), Bl, id, 1u);
+                mma_f16(d_re, sdesc(ail + ko), Bh, idn, 1u);
                 mma_f16(d_im, sdesc(arl + ko), Bh, id, 1u);
               }
             }

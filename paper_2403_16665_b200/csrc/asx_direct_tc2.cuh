@@ -30,7 +30,7 @@
 //   13     W loader: the CTA's 32 KB half of the W chunk by one bulk copy
 //   14     W relay: re-arms rank 0's "W ready" barrier once this CTA's half
 //          has landed (a bulk copy completes on a barrier of its own CTA)
-//   15-18  per-signal scales of the CTA's 64 signals, one tile ahead,
+//   15-22  per-signal scales of the CTA's 64 signals, one tile ahead,
 //          written to both CTAs' shared memory (the epilogue of each CTA
 //          scales all 128 signals of the tile)
 #pragma once
@@ -39,6 +39,12 @@
 
 #include "asx_direct_tc.cuh"
 
+#ifndef ASX_DTC2_ABLATE
+#define ASX_DTC2_ABLATE 0  // timing-only ablation builds (`make variant`, wrong results): 1 no MMAs, 2 no
+                           // epilogue stores, 4 no x loads in the converters, 8 no scale pass loads, 16 no W
+                           // bulk copies.  0 shipped.
+#endif
+
 namespace asx {
 namespace dtc2 {
 
@@ -46,14 +52,20 @@ constexpr int TS = 128;                  // signals per pair tile (MMA N)
 constexpr int HS = 64;                   // signals per CTA
 constexpr int MB = 256;                  // bins (MMA M, 128 per CTA)
 constexpr int KC = 32;                   // samples per chunk
-constexpr int NCONV = 256, NEPI = 128, NSCALE = 128;
+constexpr int NCONV = 256, NEPI = 128, NSCALE = 256;
 constexpr int WR_CONV = 0, WR_EPI = 8, WR_MMA = 12, WR_LOAD = 13, WR_RELAY = 14, WR_SCALE = 15;
-constexpr int NTHREADS = 32 * 19;
+constexpr int NTHREADS = 32 * 23;
 constexpr int X_TERM = HS * KC * 2;      // one fp16 term of 64 signals: 4 KB
 constexpr int X_STAGE = 4 * X_TERM;      // [xr hi | xr lo | xi hi | xi lo]
 constexpr int W_TERM = 128 * KC * 2;     // one fp16 term of 128 bins: 8 KB
 constexpr int W_STAGE = 4 * W_TERM;      // [Wr hi | Wr lo | Wi hi | Wi lo]
-constexpr int NX = 4, NW = 3, NSC = 3;
+#ifndef ASX_DTC2_NX
+#define ASX_DTC2_NX 4
+#endif
+#ifndef ASX_DTC2_NW
+#define ASX_DTC2_NW 3
+#endif
+constexpr int NX = ASX_DTC2_NX, NW = ASX_DTC2_NW, NSC = 3;
 constexpr int ACC_COLS = 2 * TS;         // Re | Im of one tile
 constexpr float W_SCALE = 256.0f;
 constexpr int SCALE_BYTES = NSC * TS * 16;  // float4 (f1, f2, 1/f1, 1/(f2 W_SCALE)) per signal
@@ -80,8 +92,15 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// release at cluster scope: for data the peer reads with generic loads (the
+// scales); costs a GPU-scope membar, so only once per tile
 __device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// plain remote arrive (default semantics): hand-offs whose data is read by the
+// tensor core's async proxy (after fence.proxy.async) or lives in tensor memory
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
@@ -124,14 +143,14 @@ __device__ __forceinline__ void commit2(uint64_t* bar) {
 __device__ __forceinline__ uint32_t idesc2(bool neg_a) {
   return (1u << 4) | (neg_a ? (1u << 13) : 0u) | (uint32_t(TS >> 3) << 17) | (uint32_t(MB >> 4) << 24);
 }
-// Re and Im columns of one 32-signal block, wait fused: the registers cannot
+// Re and Im columns of one 16-signal block, wait fused: the registers cannot
 // be consumed before the loads have landed
-__device__ __forceinline__ void tmem_ld_re_im(uint32_t a_re, uint32_t a_im, uint32_t (&re)[32], uint32_t (&im)[32]) {
+__device__ __forceinline__ void tmem_ld_re_im(uint32_t a_re, uint32_t a_im, uint32_t (&re)[16], uint32_t (&im)[16]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%64];\n"
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%65];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%32];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%33];\n"
       "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(re[0]), "=r"(re[1]), "=r"(re[2]), "=r"(re[3]), "=r"(re[4]), "=r"(re[5]), "=r"(re[6]), "=r"(re[7]), "=r"(re[8]), "=r"(re[9]), "=r"(re[10]), "=r"(re[11]), "=r"(re[12]), "=r"(re[13]), "=r"(re[14]), "=r"(re[15]), "=r"(re[16]), "=r"(re[17]), "=r"(re[18]), "=r"(re[19]), "=r"(re[20]), "=r"(re[21]), "=r"(re[22]), "=r"(re[23]), "=r"(re[24]), "=r"(re[25]), "=r"(re[26]), "=r"(re[27]), "=r"(re[28]), "=r"(re[29]), "=r"(re[30]), "=r"(re[31]), "=r"(im[0]), "=r"(im[1]), "=r"(im[2]), "=r"(im[3]), "=r"(im[4]), "=r"(im[5]), "=r"(im[6]), "=r"(im[7]), "=r"(im[8]), "=r"(im[9]), "=r"(im[10]), "=r"(im[11]), "=r"(im[12]), "=r"(im[13]), "=r"(im[14]), "=r"(im[15]), "=r"(im[16]), "=r"(im[17]), "=r"(im[18]), "=r"(im[19]), "=r"(im[20]), "=r"(im[21]), "=r"(im[22]), "=r"(im[23]), "=r"(im[24]), "=r"(im[25]), "=r"(im[26]), "=r"(im[27]), "=r"(im[28]), "=r"(im[29]), "=r"(im[30]), "=r"(im[31])
+      : "=r"(re[0]), "=r"(re[1]), "=r"(re[2]), "=r"(re[3]), "=r"(re[4]), "=r"(re[5]), "=r"(re[6]), "=r"(re[7]), "=r"(re[8]), "=r"(re[9]), "=r"(re[10]), "=r"(re[11]), "=r"(re[12]), "=r"(re[13]), "=r"(re[14]), "=r"(re[15]), "=r"(im[0]), "=r"(im[1]), "=r"(im[2]), "=r"(im[3]), "=r"(im[4]), "=r"(im[5]), "=r"(im[6]), "=r"(im[7]), "=r"(im[8]), "=r"(im[9]), "=r"(im[10]), "=r"(im[11]), "=r"(im[12]), "=r"(im[13]), "=r"(im[14]), "=r"(im[15])
       : "r"(a_re), "r"(a_im)
       : "memory");
 }
@@ -192,53 +211,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
 
   if (warp < WR_EPI) {
     // ------------------------------ converters ------------------------------
+    // 64 rows x 32 complex (256 B) of x per chunk; a thread takes 4 consecutive
+    // complex, twice.  The next chunk's loads (of this tile or the next) are in
+    // flight while the current one is converted.
     uint32_t cx = 0;  // x chunks produced
     const uint32_t xfull0 = mapa(smem_u32(x_full), 0);
-    int it = 0;
-    for (int64_t t = pair; t < ntiles; t += npairs, ++it) {
-      const int sb = it % NSC;
-      wait_cluster(&sc_full[sb], (it / NSC) & 1);
-      const float4* sc = scale + sb * TS + HS * rank;
-      for (int c = 0; c < kcn; ++c) {
-        const uint32_t s = cx % NX;
-        // 64 rows x 32 complex (256 B) of x; a thread takes 4 consecutive complex, twice
-        float4 v[2][2];
+    auto load = [&](int64_t t, int c, float4 (&v)[2][2]) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
-          const int64_t b = t * TS + HS * rank + row;
-          v[i][0] = v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (b < p.batch) {
-            const float4* src = reinterpret_cast<const float4*>(p.x + b * 2 * p.xs + (int64_t)c * 2 * KC) + 2 * g;
-            v[i][0] = __ldcs(src);
-            v[i][1] = __ldcs(src + 1);
-          }
+      for (int i = 0; i < 2; ++i) {
+        const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
+        const int64_t b = t * TS + HS * rank + row;
+        v[i][0] = v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < p.batch && !(ASX_DTC2_ABLATE & 4)) {
+          const float4* src = reinterpret_cast<const float4*>(p.x + b * 2 * p.xs + (int64_t)c * 2 * KC) + 2 * g;
+          v[i][0] = __ldcs(src);
+          v[i][1] = __ldcs(src + 1);
         }
-        wait_cluster(&x_empty[s], ((cx / NX) & 1) ^ 1);
-        unsigned char* st = sX + s * X_STAGE;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
-          const float4 f = sc[row];
-          const float a = f.x, bb = f.y;
-          uint2 rh, rl, ih, il;
-          dtc::split2(v[i][0].x * a * bb, v[i][0].z * a * bb, rh.x, rl.x);
-          dtc::split2(v[i][1].x * a * bb, v[i][1].z * a * bb, rh.y, rl.y);
-          dtc::split2(v[i][0].y * a * bb, v[i][0].w * a * bb, ih.x, il.x);
-          dtc::split2(v[i][1].y * a * bb, v[i][1].w * a * bb, ih.y, il.y);
-          const uint32_t off = dtc::swz(row, 4 * g);
-          *reinterpret_cast<uint2*>(st + off) = rh;
-          *reinterpret_cast<uint2*>(st + X_TERM + off) = rl;
-          *reinterpret_cast<uint2*>(st + 2 * X_TERM + off) = ih;
-          *reinterpret_cast<uint2*>(st + 3 * X_TERM + off) = il;
-        }
-        fence_proxy_async();  // generic-proxy stores -> the MMA's async-proxy reads
-        __syncwarp();
-        if (lane == 0) arrive_cluster(xfull0 + s * 8);
-        ++cx;
       }
+    };
+    float4 v[2][2], vn[2][2];
+    int64_t t = pair;
+    int c = 0, it = 0;
+    if (t < ntiles) load(t, 0, v);
+    while (t < ntiles) {
+      int64_t tn = t;
+      int cn = c + 1;
+      if (cn == kcn) {
+        cn = 0;
+        tn += npairs;
+      }
+      if (tn < ntiles) load(tn, cn, vn);
+      const int sb = it % NSC;
+      if (c == 0) wait_cluster(&sc_full[sb], (it / NSC) & 1);
+      const float4* sc = scale + sb * TS + HS * rank;
+      const uint32_t s = cx % NX;
+      mbar_wait(&x_empty[s], ((cx / NX) & 1) ^ 1);
+      unsigned char* st = sX + s * X_STAGE;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int q = tid + NCONV * i, row = q >> 3, g = q & 7;
+        const float4 f = sc[row];
+        const float a = f.x, bb = f.y;
+        uint2 rh, rl, ih, il;
+        dtc::split2(v[i][0].x * a * bb, v[i][0].z * a * bb, rh.x, rl.x);
+        dtc::split2(v[i][1].x * a * bb, v[i][1].z * a * bb, rh.y, rl.y);
+        dtc::split2(v[i][0].y * a * bb, v[i][0].w * a * bb, ih.x, il.x);
+        dtc::split2(v[i][1].y * a * bb, v[i][1].w * a * bb, ih.y, il.y);
+        const uint32_t off = dtc::swz(row, 4 * g);
+        *reinterpret_cast<uint2*>(st + off) = rh;
+        *reinterpret_cast<uint2*>(st + X_TERM + off) = rl;
+        *reinterpret_cast<uint2*>(st + 2 * X_TERM + off) = ih;
+        *reinterpret_cast<uint2*>(st + 3 * X_TERM + off) = il;
+      }
+      fence_proxy_async();  // generic-proxy stores -> the MMA's async-proxy reads
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sc_empty[sb]);
+      if (lane == 0) arrive_remote(xfull0 + s * 8);
+      ++cx;
+      if (c == kcn - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sc_empty[sb]);
+        ++it;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        v[i][0] = vn[i][0];
+        v[i][1] = vn[i][1];
+      }
+      t = tn;
+      c = cn;
     }
   } else if (warp < WR_MMA) {
     // ------------------------------ epilogue ------------------------------
@@ -250,20 +290,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
     int it = 0;
     for (int64_t t = pair; t < ntiles; t += npairs, ++it) {
       const int ab = it & 1, sb = it % NSC;
-      wait_cluster(&acc_full[ab], (it >> 1) & 1);
+      mbar_wait(&acc_full[ab], (it >> 1) & 1);
       wait_cluster(&sc_full[sb], (it / NSC) & 1);
       tmem_fence_after();
       const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(ab * ACC_COLS);
       const float4* sc = scale + sb * TS;
 #pragma unroll 1
-      for (int s0 = 0; s0 < TS; s0 += 32) {
-        uint32_t re[32], im[32];
+      for (int s0 = 0; s0 < TS; s0 += 16) {
+        uint32_t re[16], im[16];
         tmem_ld_re_im(base + (uint32_t)s0, base + (uint32_t)(TS + s0), re, im);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < 16; ++j) {
           const int64_t sig = t * TS + s0 + j;
           const float4 f = sc[s0 + j];  // broadcast read
-          if (sig < p.batch)
+          if (sig < p.batch && !(ASX_DTC2_ABLATE & 2))
             __stcs(reinterpret_cast<float2*>(p.X + sig * 2 * p.Xs) + bin,
                    make_float2(__uint_as_float(re[j]) * f.z * f.w, __uint_as_float(im[j]) * f.z * f.w));
         }
@@ -271,7 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
       tmem_fence_before();
       __syncwarp();
       if (lane == 0) {
-        arrive_cluster(acc_empty0 + ab * 8);
+        arrive_remote(acc_empty0 + ab * 8);
         mbar_arrive(&sc_empty[sb]);
         arrive_cluster(sc_empty_peer + sb * 8);
       }
@@ -285,33 +325,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
       int it = 0;
       for (int64_t t = pair; t < ntiles; t += npairs, ++it) {
         const int ab = it & 1;
-        wait_cluster(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
         tmem_fence_after();
         const uint32_t d_re = tmem + (uint32_t)(ab * ACC_COLS), d_im = d_re + (uint32_t)TS;
         for (int c = 0; c < kcn; ++c) {
           const uint32_t sw = cw % NW, sx = cx % NX;
-          wait_cluster(&w_ready[sw], (cw / NW) & 1);
-          wait_cluster(&x_full[sx], (cx / NX) & 1);
+          mbar_wait(&w_ready[sw], (cw / NW) & 1);
+          mbar_wait(&x_full[sx], (cx / NX) & 1);
           tmem_fence_after();
           const uint32_t wrh = w0 + sw * W_STAGE, wrl = wrh + W_TERM, wih = wrl + W_TERM, wil = wih + W_TERM;
           const uint32_t xrh = x0 + sx * X_STAGE, xrl = xrh + X_TERM, xih = xrl + X_TERM, xil = xih + X_TERM;
 #pragma unroll
-          for (int k = 0; k < KC / 16; ++k) {
+          for (int k = 0; k < KC / 16 && !(ASX_DTC2_ABLATE & 1); ++k) {
             const uint32_t ko = k * 32;  // 16 fp16 along the 64-byte swizzled row
             const uint32_t first = (c == 0 && k == 0) ? 0u : 1u;
-            // Re = Wr xr - Wi xi
+            // Re = Wr xr - Wi xi, Im = Wr xi + Wi xr, alternating between the two
+            // accumulators so consecutive MMAs never wait on each other's D
             mma2_f16(d_re, dtc::sdesc(wrh + ko), dtc::sdesc(xrh + ko), id, first);
-            mma2_f16(d_re, dtc::sdesc(wrh + ko), dtc::sdesc(xrl + ko), id, 1u);
-            mma2_f16(d_re, dtc::sdesc(wrl + ko), dtc::sdesc(xrh + ko), id, 1u);
-            mma2_f16(d_re, dtc::sdesc(wih + ko), dtc::sdesc(xih + ko), idn, 1u);
-            mma2_f16(d_re, dtc::sdesc(wih + ko), dtc::sdesc(xil + ko), idn, 1u);
-            mma2_f16(d_re, dtc::sdesc(wil + ko), dtc::sdesc(xih + ko), idn, 1u);
-            // Im = Wr xi + Wi xr
             mma2_f16(d_im, dtc::sdesc(wrh + ko), dtc::sdesc(xih + ko), id, first);
+            mma2_f16(d_re, dtc::sdesc(wrh + ko), dtc::sdesc(xrl + ko), id, 1u);
             mma2_f16(d_im, dtc::sdesc(wrh + ko), dtc::sdesc(xil + ko), id, 1u);
+            mma2_f16(d_re, dtc::sdesc(wrl + ko), dtc::sdesc(xrh + ko), id, 1u);
             mma2_f16(d_im, dtc::sdesc(wrl + ko), dtc::sdesc(xih + ko), id, 1u);
+            mma2_f16(d_re, dtc::sdesc(wih + ko), dtc::sdesc(xih + ko), idn, 1u);
             mma2_f16(d_im, dtc::sdesc(wih + ko), dtc::sdesc(xrh + ko), id, 1u);
+            mma2_f16(d_re, dtc::sdesc(wih + ko), dtc::sdesc(xil + ko), idn, 1u);
             mma2_f16(d_im, dtc::sdesc(wih + ko), dtc::sdesc(xrl + ko), id, 1u);
+            mma2_f16(d_re, dtc::sdesc(wil + ko), dtc::sdesc(xih + ko), idn, 1u);
             mma2_f16(d_im, dtc::sdesc(wil + ko), dtc::sdesc(xrh + ko), id, 1u);
           }
           commit2(&w_empty[sw]);
@@ -330,9 +370,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
       for (int64_t t = pair; t < ntiles; t += npairs) {
         for (int c = 0; c < kcn; ++c, ++cw) {
           const uint32_t sw = cw % NW;
-          wait_cluster(&w_empty[sw], ((cw / NW) & 1) ^ 1);
-          mbar_expect_tx(&w_full[sw], (uint32_t)W_STAGE);
-          tma_load_1d(sW + sw * W_STAGE, p.wimg + (size_t)(2 * c + rank) * W_STAGE, (uint32_t)W_STAGE, &w_full[sw]);
+          mbar_wait(&w_empty[sw], ((cw / NW) & 1) ^ 1);
+          if (ASX_DTC2_ABLATE & 16) {
+            mbar_arrive(&w_full[sw]);
+          } else {
+            mbar_expect_tx(&w_full[sw], (uint32_t)W_STAGE);
+            tma_load_1d(sW + sw * W_STAGE, p.wimg + (size_t)(2 * c + rank) * W_STAGE, (uint32_t)W_STAGE, &w_full[sw]);
+          }
         }
       }
     }
@@ -346,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
         for (int c = 0; c < kcn; ++c, ++cw) {
           const uint32_t sw = cw % NW;
           mbar_wait(&w_full[sw], (cw / NW) & 1);
-          arrive_cluster(ready0 + sw * 8);
+          arrive_remote(ready0 + sw * 8);
         }
       }
     }
@@ -354,7 +398,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
   } else {
     // ------------------ per-signal scales, one tile ahead ------------------
     // 2^e, e = 10 - ilogb(max|x|), split e = e1 + e2 (asx_direct_tc.cuh); the
-    // CTA's 64 signals, 16 per warp, four at a time with all loads in flight
+    // CTA's 64 signals, 8 per warp, four at a time with all loads in flight
+    // (this first read of x comes from HBM: eight warps keep enough of it in flight)
     const int sw = warp - WR_SCALE;
     const uint32_t sc_full_peer = mapa(smem_u32(sc_full), peer);
     int it = 0;
@@ -363,7 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
       wait_cluster(&sc_empty[sb], ((it / NSC) & 1) ^ 1);
       float4* sc = scale + sb * TS;
       const uint32_t sc_peer = mapa(smem_u32(sc), peer);
-      for (int r0 = 16 * sw; r0 < 16 * sw + 16; r0 += 4) {
+      for (int r0 = 8 * sw; r0 < 8 * sw + 8; r0 += 4) {
         float mx[4] = {0.f, 0.f, 0.f, 0.f};
         const int nq = p.n / 2;  // float4 per row
         for (int i0 = 0; i0 < nq; i0 += 128) {
@@ -375,7 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) k_direc
             for (int u = 0; u < 4; ++u) {
               const int i = i0 + lane + 32 * u;
               v[rr][u] = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (b < p.batch && i < nq) v[rr][u] = __ldg(reinterpret_cast<const float4*>(p.x + b * 2 * p.xs) + i);
+              if (b < p.batch && i < nq && !(ASX_DTC2_ABLATE & 8)) v[rr][u] = __ldg(reinterpret_cast<const float4*>(p.x + b * 2 * p.xs) + i);
             }
           }
 #pragma unroll
