@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define ASX_ABI_VERSION 1
+#define ASX_ABI_VERSION 2  /* 2: asx_plan_info.batch_group */
 
 /* Status codes mirror the reference's exception types / CLI exit codes
  * (cli.py:24-29: 3 = incompatible alpha, 4 = unsupported size). */
@@ -85,8 +85,11 @@ typedef struct asx_plan_info {
   int64_t predicted_mults; /* fastpath.py:113-121 closed form (-1 if n/a)      */
   int64_t predicted_adds;  /* fastpath.py:124-127 closed form (-1 if n/a)      */
   int64_t workspace_bytes; /* device bytes held by the plan                    */
-  int32_t kernels_per_execute; /* launches issued by one asx_execute          */
+  int32_t kernels_per_execute; /* launches issued by one asx_execute (four-step
+                                  plans: per group of batch_group signals)    */
   int32_t device;
+  int64_t batch_group;     /* four-step plans: signals per launch set (the
+                              workspace holds this many); 0 = whole batch     */
 } asx_plan_info;
 
 typedef struct asx_plan_s* asx_plan_t;

@@ -51,6 +51,7 @@ class PlanInfo(ctypes.Structure):
         ("workspace_bytes", ctypes.c_int64),
         ("kernels_per_execute", ctypes.c_int32),
         ("device", ctypes.c_int32),
+        ("batch_group", ctypes.c_int64),
     ]
 
 

@@ -101,6 +101,7 @@ struct asx_plan_s {
   int large = 0;
   int large_fft = 0;  // the α-FFT through the same four-step kernels (P = N > one CTA), one residue per launch pair
   int64_t P1 = 0, P2 = 0;
+  int64_t group = 1;  // signals per four-step launch set (the plan workspace holds group x P elements)
   int lfBig = 0;
   int row_local = 0;  // complex128 P2 = 8192: rows on k_large_rows_local, Ht stored permuted
   size_t off_twP1 = 0, off_twBig = 0, off_A = 0;
@@ -211,7 +212,7 @@ void* large_workspace(asx_plan_s* p, cudaStream_t st) {
   for (auto& kv : p->ws_extra)
     if (kv.first == st) return kv.second;
   void* w = nullptr;
-  if (cudaMalloc(&w, celem(p->dtype) * size_t(p->P)) != cudaSuccess) {
+  if (cudaMalloc(&w, celem(p->dtype) * size_t(p->P) * size_t(p->group)) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
@@ -326,27 +327,28 @@ int launch_execute(asx_plan_s* p, const void* x, int64_t xs, void* X, int64_t Xs
     lp.P2 = p->P2;
     const int dbl = p->dtype == ASX_C128;
     const size_t ie = in_elem(p), oe = celem(p->dtype);
-    if (p->large_fft) {
-      // α-FFT: one (columns, rows) launch pair per output residue c < min(r, M)
-      lp.P = p->n;
-      lp.r = p->r;
-      const int64_t nres = std::min<int64_t>(p->r, p->m);
-      for (int64_t b = 0; b < batch && e == cudaSuccess; ++b) {
-        lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
-        lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
+    lp.xs = xs;
+    lp.Xs = Xs;
+    // the batch in groups of p->group signals, one launch set per group
+    for (int64_t b = 0; b < batch && e == cudaSuccess; b += p->group) {
+      lp.nsig = std::min(p->group, batch - b);
+      lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
+      lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
+      if (p->large_fft) {
+        // α-FFT: one (columns, rows) launch pair per output residue c < min(r, M)
+        lp.P = p->n;
+        lp.r = p->r;
+        const int64_t nres = std::min<int64_t>(p->r, p->m);
         for (int64_t c = 0; c < nres && e == cudaSuccess; ++c) {
           lp.c = c;
           e = launch_large(dbl, p->P1, COL_AFFT, 0, 0, lp, st);
           if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_AFFT, 1, lp, st);
         }
+      } else {
+        e = launch_large(dbl, p->P1, COL_FWD_SIGNAL, 0, 0, lp, st);
+        if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, p->row_local ? ROW_MAIN_LOCAL : ROW_MAIN, 1, lp, st);
+        if (e == cudaSuccess) e = launch_large(dbl, p->P1, COL_INV_OUT, 0, 0, lp, st);
       }
-    }
-    for (int64_t b = 0; b < batch && e == cudaSuccess && !p->large_fft; ++b) {
-      lp.x = static_cast<const char*>(x) + (size_t)b * xs * ie;
-      lp.X = static_cast<char*>(X) + (size_t)b * Xs * oe;
-      e = launch_large(dbl, p->P1, COL_FWD_SIGNAL, 0, 0, lp, st);
-      if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, p->row_local ? ROW_MAIN_LOCAL : ROW_MAIN, 1, lp, st);
-      if (e == cudaSuccess) e = launch_large(dbl, p->P1, COL_INV_OUT, 0, 0, lp, st);
     }
   } else {
     const size_t ie = in_elem(p);
@@ -576,6 +578,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     twBig_sz = two_level_size(p->r * n, p->lfBig);  // W_{rN}: α pre-twiddle and four-step twiddle
     A_sz = n;
   }
+  // four-step workspace: group x P elements, group = the signals one launch
+  // set transforms (512 MiB of workspace, at least one signal)
   if (chosen == ASX_FFT && p->r > 1 && !p->large_fft) {
     p->lfA = two_level_lf(p->r * p->P);
     twA_sz = two_level_size(p->r * p->P, p->lfA);
@@ -592,7 +596,12 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     twP1_sz = two_level_size(p->P1, lf_of_P((int)p->P1));
     p->lfBig = two_level_lf(chirp_P);
     twBig_sz = two_level_size(chirp_P, p->lfBig);
-    A_sz = chirp_P;  // four-step workspace
+    A_sz = chirp_P;  // four-step workspace (x group, below)
+  }
+  if (p->large) {
+    const size_t per = (dbl ? sizeof(double2) : sizeof(float2)) * (size_t)A_sz;
+    p->group = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t)((512ull << 20) / per)));
+    A_sz *= p->group;
   }
   if (chosen == ASX_DIRECT) W_sz = m * n;
   if (chosen == ASX_DIRECT && dtc_ok) {
@@ -673,6 +682,7 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
         lp.scale = 1.0 / (double)chirp_P;
         lp.P = chirp_P;
         lp.P2 = p->P2;
+        lp.nsig = 1;
         e = launch_large(dbl, p->P1, COL_FWD_TABLE, 0, 0, lp, st);
         if (e == cudaSuccess) e = launch_large(dbl, p->P1, 0, ROW_SPECTRUM, 1, lp, st);
         p->row_local = (dbl && p->P2 == ChirpLocal128::P && p->env.use_local && p->env.use_tmem) ? 1 : 0;
@@ -759,6 +769,7 @@ int asx_plan_query(asx_plan_t p, asx_plan_info* info) {
   info->predicted_adds = p->pred_adds;
   info->workspace_bytes = (int64_t)p->table_bytes;
   info->kernels_per_execute = p->large_fft ? (int32_t)(2 * std::min<int64_t>(p->r, p->m)) : p->large ? 3 : 1;
+  info->batch_group = p->large ? p->group : 0;
   info->device = p->device;
   return ASX_OK;
 }

@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
   uint32_t& tmem_slot = *reinterpret_cast<uint32_t*>(war + 1);
   const int t = threadIdx.x, warp = t >> 5, j = t & 31, h = j >> 4, l = j & 15;
   const int rows = int(p.P / L::P);
+  const int64_t urows = int64_t(rows) * p.nsig;  // the group's workspaces are one [nsig * rows][P2] matrix
   const uint64_t Pmask = uint64_t(p.P - 1);
   for (int e = t; e < L::T3N; e += L::NT) {
     const int row = e / L::T3S, col = e % L::T3S;
@@ -453,13 +454,15 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
   const C* twb = reinterpret_cast<const C*>(p.twBig);
   uint32_t xcnt = 0;
 #pragma unroll 1
-  for (int k1 = blockIdx.x; k1 < rows; k1 += gridDim.x) {
-    if (t == 0 && k1 + int(gridDim.x) < rows) {
-      const int64_t nxt = int64_t(k1 + gridDim.x) * L::P;
-      prefetch_l2_bulk(reinterpret_cast<const C*>(p.A) + nxt, uint32_t(L::P * sizeof(C)));
+  for (int64_t ur = blockIdx.x; ur < urows; ur += gridDim.x) {
+    const int k1 = int(ur % rows);
+    if (t == 0 && ur + int64_t(gridDim.x) < urows) {
+      const int64_t nr = ur + int64_t(gridDim.x);
+      prefetch_l2_bulk(reinterpret_cast<const C*>(p.A) + nr * L::P, uint32_t(L::P * sizeof(C)));
+      const int64_t nxt = int64_t(nr % rows) * L::P;
       prefetch_l2_bulk(Ht + nxt, uint32_t(L::P * sizeof(C)));
     }
-    C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * L::P;
+    C* row = reinterpret_cast<C*>(p.A) + ur * L::P;
     C v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = row[t + 512 * i];

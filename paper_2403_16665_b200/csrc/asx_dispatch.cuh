@@ -345,7 +345,7 @@ cudaError_t launch_by_size(int which, int P, const KParams& kp, int64_t batch, c
 template <typename Real, int P1>
 cudaError_t launch_cols(int mode, const LParams& lp, cudaStream_t st) {
   using G = ColCfg<Real, P1>;
-  const int64_t tiles = lp.P2 / kColTile;
+  const int64_t tiles = (lp.P2 / kColTile) * std::max<int64_t>(lp.nsig, 1);
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kern) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
@@ -406,7 +406,7 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       cudaGetLastError();
-    if (e == cudaSuccess) kern<<<(unsigned)std::min<int64_t>(P1, sms), G::NT, smem, st>>>(lp);
+    if (e == cudaSuccess) kern<<<(unsigned)std::min<int64_t>(P1 * std::max<int64_t>(lp.nsig, 1), sms), G::NT, smem, st>>>(lp);
   };
   if constexpr (sizeof(Real) == 8) {
     if (mode == ROW_MAIN_LOCAL) {
@@ -415,7 +415,9 @@ cudaError_t launch_rows(int mode, int64_t P1, const LParams& lp, cudaStream_t st
       int sms = 148, dev = 0;
       if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         cudaGetLastError();
-      if (e == cudaSuccess) kern<<<(unsigned)std::min<int64_t>(P1, sms), ChirpLocal128::NT, RowsLocal::SMEM, st>>>(lp);
+      if (e == cudaSuccess)
+        kern<<<(unsigned)std::min<int64_t>(P1 * std::max<int64_t>(lp.nsig, 1), sms), ChirpLocal128::NT, RowsLocal::SMEM,
+               st>>>(lp);
       if (e != cudaSuccess) return e;
       return cudaGetLastError();
     }

@@ -63,6 +63,8 @@ struct LParams {
   int64_t P;            // P1 * P2
   int64_t P2;           // row length (row stride of A / Ht)
   int64_t r, c;         // α-FFT modes: density r (power of two), residue c; twBig = W_{rN}
+  int64_t nsig;         // signals per launch (batched: workspace [nsig][P], x / X rows at xs / Xs)
+  int64_t xs, Xs;       // row strides of x and X (elements)
 };
 
 template <typename C>
@@ -107,9 +109,14 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   // persistent over column tiles: the per-CTA twiddle setup (make_tw, FP64
   // sincospi seeds) is paid once per CTA instead of once per tile
   const int ntiles = int(P2 / kColTile);
+  const int64_t units = int64_t(ntiles) * p.nsig;  // (signal, column tile) pairs of the group
 #pragma unroll 1
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int col0 = tile * kColTile;
+  for (int64_t un = blockIdx.x; un < units; un += gridDim.x) {
+    const int64_t g = un / ntiles;
+    const int col0 = int(un - g * ntiles) * kColTile;
+    const void* xg = static_cast<const char*>(p.x) + g * p.xs * (p.real_in ? sizeof(Real) : sizeof(C));
+    C* const Ag = reinterpret_cast<C*>(p.A) + g * p.P;
+    C* const Xg = reinterpret_cast<C*>(p.X) + g * p.Xs;
     __syncthreads();  // the previous tile's write-out reads of smbase are done
     // ---- gather the column tile: kColTile threads per row, rows strided ----
     {
@@ -119,21 +126,21 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
         C val = mk(Real(0), Real(0));
         if constexpr (MODE == COL_FWD_SIGNAL) {
           if (idx < p.n) {  // y[n] = x[n] * chirp[n], zero past N
-            const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(p.x) + idx), Real(0))
-                                   : __ldg(reinterpret_cast<const C*>(p.x) + idx);
+            const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(xg) + idx), Real(0))
+                                   : __ldg(reinterpret_cast<const C*>(xg) + idx);
             val = cmul(xv, __ldg(reinterpret_cast<const C*>(p.chirp) + idx));
           }
         } else if constexpr (MODE == COL_FWD_TABLE) {
           val = __ldg(reinterpret_cast<const C*>(p.h) + idx);
         } else if constexpr (MODE == COL_AFFT) {
           // x[P2 n1 + n2] × W_{rP1}^{c n1} = W_{rN}^{c n1 P2}
-          const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(p.x) + idx), Real(0))
-                                 : __ldg(reinterpret_cast<const C*>(p.x) + idx);
+          const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(xg) + idx), Real(0))
+                                 : __ldg(reinterpret_cast<const C*>(xg) + idx);
           val = p.c ? cmul(xv, tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(p.c) * uint64_t(row) *
                                                                           uint64_t(P2)) & Pmask, p.lfBig))
                     : xv;
         } else {
-          val = __ldg(reinterpret_cast<const C*>(p.A) + idx);  // B[k1][c], row = k1
+          val = __ldg(Ag + idx);  // B[k1][c], row = k1
         }
         smbase[tau * CS + E::pad(row)] = val;
       }
@@ -171,11 +178,11 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
       for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
         const C val = smbase[tau * CS + E::pad(row)];
         if constexpr (MODE != COL_INV_OUT) {
-          reinterpret_cast<C*>(p.A)[int64_t(row) * P2 + col0 + tau] = val;
+          Ag[int64_t(row) * P2 + col0 + tau] = val;
         } else {
           const int64_t mm = int64_t(col0 + tau) + P2 * row;  // m = c + P2 d
           if (mm < p.m)
-            reinterpret_cast<C*>(p.X)[mm] = cmul(cconj(val), __ldg(reinterpret_cast<const C*>(p.chirp) + mm));
+            Xg[mm] = cmul(cconj(val), __ldg(reinterpret_cast<const C*>(p.chirp) + mm));
         }
       }
     }
@@ -202,19 +209,22 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
   C* sm = reinterpret_cast<C*>(smraw);
   const int t = threadIdx.x;
   const int rows = int(p.P / P2);
+  const int64_t urows = int64_t(rows) * p.nsig;  // the group's workspaces are one [nsig * rows][P2] matrix
   const typename E::TwRegs tr =
       E::make_tw(t, reinterpret_cast<const C*>(p.twP2), sm + E::SMEM_ELEMS, threadIdx.x, NT);
   typename E::XSync xs;
   E::xs_init(xs, reinterpret_cast<uint64_t*>(sm + E::SMEM_ELEMS + E::TAB_ELEMS + (E::TAB_ELEMS & 1)), NT);
   __syncthreads();
 #pragma unroll 1
-  for (int k1 = blockIdx.x; k1 < rows; k1 += gridDim.x) {
-    if (t == 0 && k1 + int(gridDim.x) < rows) {
-      const int64_t nxt = int64_t(k1 + gridDim.x) * P2;
-      prefetch_l2_bulk(reinterpret_cast<const C*>(p.A) + nxt, ROW_BYTES);
-      if (MODE == ROW_MAIN) prefetch_l2_bulk(reinterpret_cast<const C*>(p.Ht) + nxt, ROW_BYTES);
+  for (int64_t ur = blockIdx.x; ur < urows; ur += gridDim.x) {
+    const int k1 = int(ur % rows);
+    const int64_t g = ur / rows;
+    if (t == 0 && ur + int64_t(gridDim.x) < urows) {
+      const int64_t nr = ur + int64_t(gridDim.x);
+      prefetch_l2_bulk(reinterpret_cast<const C*>(p.A) + nr * P2, ROW_BYTES);
+      if (MODE == ROW_MAIN) prefetch_l2_bulk(reinterpret_cast<const C*>(p.Ht) + (nr % rows) * P2, ROW_BYTES);
     }
-    C* row = reinterpret_cast<C*>(p.A) + int64_t(k1) * P2;
+    C* row = reinterpret_cast<C*>(p.A) + ur * P2;
     C v[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = row[t + NT * i];
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
       // X[c + r (d1 + P1 d2)], d1 = k1, d2 = t + NT*i; bins past M are not stored
       E::run(v, sm, t, tr, xs);
       const int64_t P1 = p.P / P2;
-      C* X = reinterpret_cast<C*>(p.X);
+      C* X = reinterpret_cast<C*>(p.X) + g * p.Xs;
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         const int64_t mm = p.c + p.r * (int64_t(k1) + P1 * int64_t(t + NT * i));

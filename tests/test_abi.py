@@ -21,7 +21,7 @@ def _declared():
 
 def test_library_present_and_loads():
     assert os.path.exists(_lib.LIB_PATH), "build libasx.so first (__graft_entry__.build())"
-    assert _lib.lib().asx_version() == 1
+    assert _lib.lib().asx_version() == 2
 
 
 def test_every_header_symbol_exported_with_matching_arity():

@@ -436,3 +436,27 @@ def test_leading_dims_flatten_into_the_batch(asx, torch):
     got_h = p.execute_host(x)
     assert got_h.shape == (2, 3, 256)
     assert orc.rel_err(got_h.reshape(6, 256), want.reshape(6, 256)) <= TOL64
+
+
+def test_four_step_batched_groups(asx, torch):
+    """The four-step path transforms the batch in groups of batch_group
+    signals per launch set (workspace group x P): complex128 N = 8192,
+    alpha = 1/8 (config 4's shape at FP64), 4096 signals = 2 groups of 2048,
+    every signal against the single-CTA alpha-FFT recursion; plus a batched
+    large alpha-FFT against the zero-padded FFT."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn((4096, 8192), dtype=torch.complex128, device="cuda", generator=g)
+    p = asx.plan(8192, asx.DenseFactor(8), m=8192, dtype="complex128", method="chirp")
+    assert p.info.kernels_per_execute == 3 and p.info.batch_group == 2048
+    q = asx.plan(8192, asx.DenseFactor(8), m=8192, dtype="complex128", method="fft")
+    got, want = p.execute(x), q.execute(x)
+    err = ((got - want).abs().amax(dim=1) / want.abs().amax(dim=1)).max().item()
+    assert err <= 2 * TOL64, err
+    # ragged batch across the group boundary, strided rows
+    sub = x[5:2060]
+    assert torch.equal(p.execute(sub), got[5:2060])
+    rng = np.random.default_rng(3)
+    xs = np.stack([orc.unit_disk(rng, 16384) for _ in range(5)])
+    got2, p2 = gpu_run(asx, xs, 1, 2, 16384, "fft")
+    assert p2.info.batch_group >= 5
+    assert orc.rel_err(got2, np.fft.fft(xs, 2 * 16384, axis=1)[:, :16384]) <= TOL64
