@@ -87,7 +87,21 @@ __device__ __forceinline__ void afl_twiddle(double2 (&v)[16], uint32_t col) {
   }
 }
 
+// Timing diagnostics (variant builds only, -DASX_AFL_TIMELINE=<iteration>): warp
+// leaders of CTA 0 stamp clock64() at the phase boundaries of two consecutive
+// signals into the row AFTER the last output row (the caller allocates it).
+#ifdef ASX_AFL_TIMELINE
+#define AFL_TL(i)                                                                                   \
+  do {                                                                                              \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (it == ASX_AFL_TIMELINE || it == ASX_AFL_TIMELINE + 1)) \
+      cx.tl[((it - ASX_AFL_TIMELINE) * 16 + (threadIdx.x >> 5)) * 16 + (i)] = clock64();           \
+  } while (0)
+#else
+#define AFL_TL(i)
+#endif
+
 struct AflCtx {
+  unsigned long long* tl;
   double2* xb;  // this team's exchange buffer
   const unsigned char* stage;
   uint64_t *full, *consumed, *war;
@@ -121,9 +135,11 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   using C = double2;
   const int t = cx.t, n0 = t & 15, hi = t >> 4;
   C v[16];
+  AFL_TL(0);
   if (live) {
     mbar_wait(cx.full, phase);
     phase ^= 1;
+    AFL_TL(1);
     const C* row = reinterpret_cast<const C*>(cx.stage);
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = row[t + 256 * i];
@@ -133,6 +149,7 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   }
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(cx.consumed);  // this warp is done with the staged row
+  AFL_TL(2);
   // ---- S1: × W_32^{c n2}, radix-16 over n2, × W_8192^{t (c + 2 g0)}
   if constexpr (CR == 1) {
 #pragma unroll
@@ -140,6 +157,7 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   }
   dft_reg<16>(v);
   afl_twiddle<CR == 0 ? 1 : 0>(v, cx.tbase);
+  AFL_TL(3);
   if (xcnt) {
     // the previous signal's bins, parked by both teams long ago: write them now,
     // between this signal's butterflies and its first exchange
@@ -148,12 +166,16 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
   }
+  AFL_TL(4);
   // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's output reads
   if (xcnt) mbar_wait(cx.war, (xcnt - 1) & 1);
+  AFL_TL(5);
   C* const xb = cx.xb;
 #pragma unroll
   for (int g0 = 0; g0 < 16; ++g0) xb[t + L::RS * g0] = v[g0];
+  AFL_TL(6);
   asm volatile("bar.sync %0, 256;" ::"r"(1 + CR) : "memory");
+  AFL_TL(7);
   if (CR == 0 && t == 0 && u + stride < int(p.batch)) {
     // next row: both teams started this signal together and have read it by now
     mbar_wait(cx.consumed, it & 1);
@@ -167,9 +189,11 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
 #pragma unroll
   for (int n1 = 0; n1 < 16; ++n1) v[n1] = rg[n0 + 16 * n1];
   __syncwarp();
+  AFL_TL(8);
   // ---- S2: radix-16 over n1, × W_256^{n0 g1}
   dft_reg<16>(v);
   afl_twiddle<1>(v, cx.tbase + 64);
+  AFL_TL(9);
   // ---- E2 (half-warp): (n0, g1) -> thread (g1 = t & 15, g0)
 #pragma unroll
   for (int g1 = 0; g1 < 16; ++g1) rg[n0 + 17 * g1] = v[g1];
@@ -177,12 +201,15 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = rg[j + 17 * n0];
   __syncwarp();
+  AFL_TL(10);
   // ---- S3: radix-16 over n0 -> g2; park bins d = hi + 16 n0 + 256 g2 < 2048
   dft_reg<16>(v);
+  AFL_TL(11);
 #pragma unroll
   for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(CR, hi, n0, g2)] = v[g2];
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(cx.parked);
+  AFL_TL(12);
 }
 
 // Launch: grid <= #SMs, NTH threads, AfftLocal::SMEM dynamic shared memory.
@@ -207,6 +234,7 @@ __global__ void __launch_bounds__(512, 1) k_afft_local(KParams p) {
   cx.parked = bars + 4;
   cx.xb0 = xb0;
   cx.t = tid & 255;
+  cx.tl = reinterpret_cast<unsigned long long*>(reinterpret_cast<C*>(p.X) + int64_t(p.batch) * p.Xs);
   const int stride = int(gridDim.x);
   int u = int(blockIdx.x);
   const int batch = int(p.batch);

@@ -694,12 +694,17 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
         }
         cudaFreeAsync(hbuf, st);
       }
-    } else if ((e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), 2 * sizeof(double2) * p->P, st)) ==
+    } else if ((e = cudaMallocAsync(reinterpret_cast<void**>(&wP_d), 3 * sizeof(double2) * p->P, st)) ==
                cudaSuccess) {
-      double2* h_d = wP_d + p->P;
+      // H = FFT(h)/P in FP64: log2 P radix-2 Stockham levels against the exact W_P table
+      double2 *src = wP_d + p->P, *dst = wP_d + 2 * p->P;
       k_fill_roots<<<(p->P + 255) / 256, 256, 0, st>>>(wP_d, p->P, 1, (uint64_t)p->P, 1);
-      k_chirp_kernel_fp64<<<(p->P + 255) / 256, 256, 0, st>>>(h_d, p->P, n, m, (uint64_t)a, L2);
-      k_chirp_spectrum<<<(p->P + 127) / 128, 128, 0, st>>>(base + p->off_H, p->P, h_d, wP_d, dbl);
+      k_chirp_kernel_fp64<<<(p->P + 255) / 256, 256, 0, st>>>(src, p->P, n, m, (uint64_t)a, L2);
+      for (int s = 1; s < p->P; s <<= 1) {
+        k_stockham2_level<<<(p->P / 2 + 255) / 256, 256, 0, st>>>(src, dst, p->P, s, wP_d);
+        std::swap(src, dst);
+      }
+      k_store_scaled<<<(p->P + 255) / 256, 256, 0, st>>>(base + p->off_H, p->P, src, dbl);
       cudaFreeAsync(wP_d, st);
     }
   }

@@ -108,6 +108,19 @@ __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
 }
 
+// Timing diagnostics (variant builds only, -DASX_CL_TIMELINE=<iteration>): warp
+// leaders of CTA 0 stamp clock64() at the phase boundaries of two consecutive
+// signals into the row AFTER the last output row (the caller allocates it).
+#ifdef ASX_CL_TIMELINE
+#define CL_TL(i)                                                                                  \
+  do {                                                                                            \
+    if (blockIdx.x == 0 && (t & 31) == 0 && (it == ASX_CL_TIMELINE || it == ASX_CL_TIMELINE + 1)) \
+      tl[((it - ASX_CL_TIMELINE) * 32 + warp) * 32 + (i)] = clock64();                            \
+  } while (0)
+#else
+#define CL_TL(i)
+#endif
+
 template <typename Real>
 __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
   using C = typename CT<Real>::T;
@@ -228,16 +241,21 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
   const bool fast_out = p.m >= L::P / 2;
   C* const rg = xb + gk * L::REG;             // this group's region
   C* const sb = rg + k2 * L::SUB;             // this half-warp's sub-block
+#ifdef ASX_CL_TIMELINE
+  unsigned long long* const tl = reinterpret_cast<unsigned long long*>(reinterpret_cast<C*>(p.X) + int64_t(p.batch) * p.Xs);
+#endif
 
 #pragma unroll 1
   for (int it = 0; it < iters; ++it, u += stride) {
     const bool live = u < batch;
     const int64_t row_off = int64_t(u) * p.xs;
     C v[16];
+    CL_TL(0);
     if (staged && live) {
       mbar_wait(stbar, phase);
       phase ^= 1;
     }
+    CL_TL(1);
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = mk(Real(0), Real(0));
 #pragma unroll
@@ -255,6 +273,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
         }
       }
     }
+    CL_TL(2);
     // ---- P1: radix-16 DIF over x[t + 1024 i] (upper half zero), twiddle W_16384^{t k1}
     dft_reg<16>(v);
     {
@@ -262,13 +281,17 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       tw_p1(w);
       tw16_apply(v, w);
     }
+    CL_TL(3);
     // ---- G1: y_k1[t] -> region k1 (WAR: previous signal's Q4 reads)
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+    CL_TL(4);
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) xb[k1 * L::REG + L::pos(t)] = v[k1];
     C tw2[12];
     ld_t2(tw2);
+    CL_TL(5);
     __syncthreads();  // G1 RAW; also: every thread has consumed the staged row
+    CL_TL(6);
     if (staged && t == 0 && u + stride < batch) {
       fence_proxy_async();
       mbar_expect_tx(stbar, (uint32_t)row_bytes);
@@ -280,6 +303,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int i = 0; i < 4; ++i) ld_pair(rg + 2 * tau + 128 * h + L::SUB * i, v[4 * (2 * h) + i], v[4 * (2 * h + 1) + i]);
+    CL_TL(7);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       dft_reg<4>(reinterpret_cast<C(&)[4]>(v[4 * g]));
@@ -291,12 +315,16 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int j = 0; j < 4; ++j) st_pair(rg + j * L::SUB + 2 * tau + 128 * h, v[4 * (2 * h) + j], v[4 * (2 * h + 1) + j]);
+    CL_TL(8);
     group_bar(gbar);  // RAW
+    CL_TL(9);
     // ---- P3: radix-16 DIF over z_{k,k2}[n'' + 16 i'']; twiddle W_256^{n'' k3}
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = sb[n16 + 16 * i];
+    CL_TL(10);
     dft_reg<16>(v);
     tw_p3(v);
+    CL_TL(11);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; ++j) sb[L::L2S * j + n16] = v[j];
@@ -311,6 +339,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
         v[2 * q + 1] = mk(Real(w.z), Real(w.w));
       }
     }
+    CL_TL(12);
     dft_reg<16>(v);
 #pragma unroll
     for (int j0 = 0; j0 < 16; j0 += CPC) {
@@ -320,7 +349,9 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       for (int k = 0; k < CPC; ++k) v[j0 + k] = cconj(cmul(v[j0 + k], hw[k]));
     }
     // ---- inverse = conj(DFT(conj(.))), DFT as the transposed passes Q1..Q4
+    CL_TL(13);
     dft_reg<16>(v);  // Q1 = P4^T
+    CL_TL(14);
     __syncwarp();
     {
       float4* row = reinterpret_cast<float4*>(sb + L::L2S * n16);
@@ -330,17 +361,22 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = sb[L::L2S * j + n16];
+    CL_TL(15);
     tw_p3(v);  // Q2 = P3^T
     dft_reg<16>(v);
+    CL_TL(16);
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 16; ++i) sb[n16 + 16 * i] = v[i];
     ld_t2(tw2);
+    CL_TL(17);
     group_bar(gbar);  // RAW
+    CL_TL(18);
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int j = 0; j < 4; ++j) ld_pair(rg + j * L::SUB + 2 * tau + 128 * h, v[4 * (2 * h) + j], v[4 * (2 * h + 1) + j]);
+    CL_TL(19);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // Q3 = P2^T
 #pragma unroll
@@ -354,14 +390,18 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
       for (int i = 0; i < 4; ++i) st_pair(rg + 2 * tau + 128 * h + L::SUB * i, v[4 * (2 * h) + i], v[4 * (2 * h + 1) + i]);
     C tw1[8];
     tw_p1(tw1);
+    CL_TL(20);
     __syncthreads();
+    CL_TL(21);
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) v[k1] = xb[k1 * L::REG + L::pos(t)];
     __syncwarp();
+    CL_TL(22);
     if ((t & 31) == 0) mbar_arrive(war);
     ++xcnt;
     tw16_apply(v, tw1);
     dft_reg<16>(v);
+    CL_TL(23);
     {
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
 #pragma unroll
@@ -380,6 +420,7 @@ __global__ void __launch_bounds__(1024, 1) k_chirp_local(KParams p) {
         }
       }
     }
+    CL_TL(24);
   }
   tmem_fence_before();
   __syncthreads();
