@@ -41,6 +41,22 @@
                           // epilogue drain, 4 no x loads in the converters.  0 in the shipped library.
 #endif
 
+// Wait accounting (variant builds only, -DASX_DTC_WAITS; scripts/dtc_waits.py):
+// one thread per role of CTA 0 sums the cycles it spends in each mbarrier wait
+// and writes them behind the last output row (the caller allocates it) as
+// int64 [role * 8 + counter]; the converter thread also records clock64 and
+// %globaltimer over the kernel (the SM clock under this kernel's power draw).
+#ifdef ASX_DTC_WAITS
+#define DTC_W(ctr, stmt)                   \
+  do {                                     \
+    const long long t0_ = clock64();       \
+    stmt;                                  \
+    ctr += clock64() - t0_;                \
+  } while (0)
+#else
+#define DTC_W(ctr, stmt) stmt
+#endif
+
 namespace asx {
 namespace dtc {
 
@@ -163,9 +179,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   uint64_t* a_empty = a_full + NA;     // NA, tcgen05.commit
   uint64_t* b_full = a_empty + NA;     // NB, TMA tx
   uint64_t* b_empty = b_full + NB;     // NB, tcgen05.commit
-  uint64_t* acc_full = b_empty + NB;   // tcgen05.commit
-  uint64_t* acc_empty = acc_full + 1;  // count NCONV
-  uint64_t* sc_full = acc_empty + 1;   // 2, count NSCALE
+  uint64_t* acc_full = b_empty + NB;   // 2 (bin halves), tcgen05.commit
+  uint64_t* acc_empty = acc_full + 2;  // 2 (bin halves), count NCONV
+  uint64_t* sc_full = acc_empty + 2;   // 2, count NSCALE
   uint64_t* sc_empty = sc_full + 2;    // 2, count NCONV
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sc_empty + 2);
   // per-signal power-of-two scale 2^e as two factors 2^e1 * 2^e2 (each in the
@@ -173,6 +189,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
   float2* scale = reinterpret_cast<float2*>(sB + NB * B_STAGE + 512);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef ASX_DTC_WAITS
+  long long* const dbg = reinterpret_cast<long long*>(p.X + p.batch * 2 * p.Xs);
+  long long w0 = 0, w1 = 0, w2 = 0, w3 = 0, wld = 0;
+  const long long t_start = clock64();
+  unsigned long long g_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+#endif
   const int kcn = p.n / KC;                 // K chunks
   const int m = p.m;
   const int b_bytes = 2 * m * KC * 2;       // one part [hi | lo]
@@ -187,8 +210,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, NCONV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], NCONV);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sc_full[i], NSCALE);
       mbar_init(&sc_empty[i], NCONV);
@@ -223,7 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
           v[i][1] = __ldcs(src + 1);
         }
       }
-      mbar_wait(&a_empty[s], ((ca / NA) & 1) ^ 1);
+      DTC_W(w1, mbar_wait(&a_empty[s], ((ca / NA) & 1) ^ 1));
       unsigned char* st = sA + s * A_STAGE;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -247,45 +272,53 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     // Re in TMEM columns [0, m), Im in [m, 2m); warp (q, h) drains lanes
     // 32q..32q+31 (its signals) and bins [h m/2, (h+1) m/2)
     auto epilogue = [&](int64_t t, int buf) {
-      mbar_wait(acc_full, ntile_done & 1);
-      tmem_fence_after();
       const int q = warp & 3, h = warp >> 2;
       // 16x256b fragments straight to global: thread t of the warp holds lanes
       // (signals) t/4 and t/4 + 8 of a 16-lane half, bins 8j + 2(t%4) + {0, 1}
-      // of a 32-bin block; each store writes 8 signals' 64-byte row segments
+      // of a 32-bin block; each store writes 8 signals' 64-byte row segments.
+      // All eight warps drain bin half 0 first (the MMA issuer re-uses those
+      // columns as soon as they are free), then half 1; warp (q, h) takes
+      // signals 32q.. and the h-th quarter of the bins of each half.
       const int64_t b0 = t * TS + q * 32;
-      for (int hl = 0; hl < 2 && !(ASX_DTC_ABLATE & 2); ++hl) {
-        const uint32_t la = tmem + ((uint32_t)(q * 32 + 16 * hl) << 16);
-        // exact inverse of 2^e1 * 2^e2 * W_SCALE, again as two normal factors
-        const float2 s0 = scale[buf * TS + q * 32 + 16 * hl + (lane >> 2)];
-        const float2 s1 = scale[buf * TS + q * 32 + 16 * hl + 8 + (lane >> 2)];
-        const float inv0a = 1.f / s0.x, inv0b = 1.f / (s0.y * W_SCALE);
-        const float inv1a = 1.f / s1.x, inv1b = 1.f / (s1.y * W_SCALE);
-        const int64_t r0 = b0 + 16 * hl + (lane >> 2), r1 = r0 + 8;
-        for (int c0 = h * (m / 2); c0 < (h + 1) * (m / 2); c0 += 32) {
-          uint32_t re[16], im[16];
-          tmem_ld16x256(la + (uint32_t)c0, re);
-          tmem_ld16x256(la + (uint32_t)(m + c0), im);
-          tmem_wait_ld(re, im);
+      for (int half = 0; half < 2; ++half) {
+        DTC_W(w2, mbar_wait(&acc_full[half], ntile_done & 1));
+        tmem_fence_after();
+        for (int hl = 0; hl < 2 && !(ASX_DTC_ABLATE & 2); ++hl) {
+          const uint32_t la = tmem + ((uint32_t)(q * 32 + 16 * hl) << 16);
+          // exact inverse of 2^e1 * 2^e2 * W_SCALE, again as two normal factors
+          const float2 s0 = scale[buf * TS + q * 32 + 16 * hl + (lane >> 2)];
+          const float2 s1 = scale[buf * TS + q * 32 + 16 * hl + 8 + (lane >> 2)];
+          const float inv0a = 1.f / s0.x, inv0b = 1.f / (s0.y * W_SCALE);
+          const float inv1a = 1.f / s1.x, inv1b = 1.f / (s1.y * W_SCALE);
+          const int64_t r0 = b0 + 16 * hl + (lane >> 2), r1 = r0 + 8;
+          const int cbeg = half * (m / 2) + h * (m / 4);
+          for (int c0 = cbeg; c0 < cbeg + m / 4; c0 += 32) {
+            uint32_t re[16], im[16];
+            DTC_W(wld, {
+              tmem_ld16x256(la + (uint32_t)c0, re);
+              tmem_ld16x256(la + (uint32_t)(m + c0), im);
+              tmem_wait_ld(re, im);
+            });
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int bin = c0 + 8 * j + 2 * (lane & 3);
-            if (r0 < p.batch)
-              __stcs(reinterpret_cast<float4*>(p.X + r0 * 2 * p.Xs + 2 * bin),
-                     make_float4(__uint_as_float(re[4 * j]) * inv0a * inv0b, __uint_as_float(im[4 * j]) * inv0a * inv0b,
-                                 __uint_as_float(re[4 * j + 1]) * inv0a * inv0b,
-                                 __uint_as_float(im[4 * j + 1]) * inv0a * inv0b));
-            if (r1 < p.batch)
-              __stcs(reinterpret_cast<float4*>(p.X + r1 * 2 * p.Xs + 2 * bin),
-                     make_float4(__uint_as_float(re[4 * j + 2]) * inv1a * inv1b,
-                                 __uint_as_float(im[4 * j + 2]) * inv1a * inv1b,
-                                 __uint_as_float(re[4 * j + 3]) * inv1a * inv1b,
-                                 __uint_as_float(im[4 * j + 3]) * inv1a * inv1b));
+            for (int j = 0; j < 4; ++j) {
+              const int bin = c0 + 8 * j + 2 * (lane & 3);
+              if (r0 < p.batch)
+                __stcs(reinterpret_cast<float4*>(p.X + r0 * 2 * p.Xs + 2 * bin),
+                       make_float4(__uint_as_float(re[4 * j]) * inv0a * inv0b, __uint_as_float(im[4 * j]) * inv0a * inv0b,
+                                   __uint_as_float(re[4 * j + 1]) * inv0a * inv0b,
+                                   __uint_as_float(im[4 * j + 1]) * inv0a * inv0b));
+              if (r1 < p.batch)
+                __stcs(reinterpret_cast<float4*>(p.X + r1 * 2 * p.Xs + 2 * bin),
+                       make_float4(__uint_as_float(re[4 * j + 2]) * inv1a * inv1b,
+                                   __uint_as_float(im[4 * j + 2]) * inv1a * inv1b,
+                                   __uint_as_float(re[4 * j + 3]) * inv1a * inv1b,
+                                   __uint_as_float(im[4 * j + 3]) * inv1a * inv1b));
+            }
           }
         }
+        tmem_fence_before();
+        mbar_arrive(&acc_empty[half]);
       }
-      tmem_fence_before();
-      mbar_arrive(acc_empty);
       mbar_arrive(&sc_empty[buf]);
       ++ntile_done;
     };
@@ -293,67 +326,118 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     for (int64_t t = blockIdx.x;; t += gridDim.x, ++it) {
       const bool valid = t < ntiles;
       if (valid) {
-        mbar_wait(&sc_full[it & 1], (it >> 1) & 1);
-        for (int c = 0; c < NA && c < kcn; ++c) convert(t, it & 1, c);
+        DTC_W(w0, mbar_wait(&sc_full[it & 1], (it >> 1) & 1));
+        // chunk 0 only: its A stage was released by the previous tile's chunk
+        // kcn - 2; chunk 1 re-uses the LAST chunk's stage and would hold the
+        // epilogue back until every MMA of the previous tile has completed
+        convert(t, it & 1, 0);
       }
-      if (prev >= 0) epilogue(prev, (it - 1) & 1);
+      if (prev >= 0) DTC_W(w3, epilogue(prev, (it - 1) & 1));
       if (!valid) break;
-      for (int c = NA; c < kcn; ++c) convert(t, it & 1, c);
+      for (int c = 1; c < kcn; ++c) convert(t, it & 1, c);
       prev = t;
     }
+#ifdef ASX_DTC_WAITS
+    if (blockIdx.x == 0 && tid == 0) {
+      unsigned long long g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      dbg[0] = w0, dbg[1] = w1, dbg[2] = w2, dbg[3] = w3, dbg[4] = clock64() - t_start, dbg[5] = it;
+      dbg[6] = (long long)(g_end - g_start), dbg[7] = wld;
+    }
+#endif
   } else if (warp == 8) {
     // ------------------------------ MMA issuer ------------------------------
     if (lane == 0) {
+#ifdef ASX_DTC_WAITS
+      w0 = w1 = w2 = 0;
+#endif
       uint32_t ca = 0, cb = 0, nt = 0;
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       const uint32_t id = idesc(m, false), idn = idesc(m, true);
+      const uint32_t idh = idesc(m / 2, false), idhn = idesc(m / 2, true);
       const uint32_t d_re = tmem, d_im = tmem + (uint32_t)m;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
-        if (nt > 0) {
-          mbar_wait(acc_empty, (nt - 1) & 1);
-          tmem_fence_after();
+      // the 12 MMAs of one 16-sample step of a part (0: Wr, 1: Wi) on N columns
+      // at accumulator column offset dc; Re / Im accumulators alternate
+      auto step = [&](int part, uint32_t arh, uint32_t arl, uint32_t aih, uint32_t ail, uint64_t Bh, uint64_t Bl,
+                      uint32_t dc, uint32_t idp, uint32_t idm, uint32_t first) {
+        if (ASX_DTC_ABLATE & 1) return;
+        if (part == 0) {  // Re += Ar Wr,  Im += Ai Wr
+          mma_f16(d_re + dc, sdesc(arh), Bh, idp, first);
+          mma_f16(d_im + dc, sdesc(aih), Bh, idp, first);
+          mma_f16(d_re + dc, sdesc(arh), Bl, idp, 1u);
+          mma_f16(d_im + dc, sdesc(aih), Bl, idp, 1u);
+          mma_f16(d_re + dc, sdesc(arl), Bh, idp, 1u);
+          mma_f16(d_im + dc, sdesc(ail), Bh, idp, 1u);
+        } else {  // Re -= Ai Wi,  Im += Ar Wi
+          mma_f16(d_re + dc, sdesc(aih), Bh, idm, 1u);
+          mma_f16(d_im + dc, sdesc(arh), Bh, idp, 1u);
+          mma_f16(d_re + dc, sdesc(aih), Bl, idm, 1u);
+          mma_f16(d_im + dc, sdesc(arh), Bl, idp, 1u);
+          mma_f16(d_re + dc, sdesc(ail), Bh, idm, 1u);
+          mma_f16(d_im + dc, sdesc(arl), Bh, idp, 1u);
         }
+      };
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         for (int c = 0; c < kcn; ++c) {
           const uint32_t sa = ca % NA;
-          mbar_wait(&a_full[sa], (ca / NA) & 1);
+          DTC_W(w1, mbar_wait(&a_full[sa], (ca / NA) & 1));
           tmem_fence_after();
           const uint32_t arh = a0 + sa * A_STAGE, arl = arh + A_TERM, aih = arl + A_TERM, ail = aih + A_TERM;
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {  // 0: Wr, 1: Wi
-            const uint32_t sb = cb % NB;
-            mbar_wait(&b_full[sb], (cb / NB) & 1);
+          if (c == 0 || c == kcn - 1) {
+            // First and last chunk of a tile run as two bin halves (N = m / 2):
+            // the accumulator fills all of tensor memory, so the previous tile's
+            // epilogue cannot overlap whole-width MMAs; per half, the last chunk's
+            // half 0 is committed (and drained) while half 1 still multiplies, and
+            // the next tile's half 0 starts as soon as ITS columns are drained.
+            const uint32_t sb0 = cb % NB, sb1 = (cb + 1) % NB;
+            DTC_W(w2, mbar_wait(&b_full[sb0], (cb / NB) & 1));
+            DTC_W(w2, mbar_wait(&b_full[sb1], ((cb + 1) / NB) & 1));
             tmem_fence_after();
-            const uint32_t bh = b0 + sb * B_STAGE, bl = bh + (uint32_t)(b_bytes / 2);
 #pragma unroll
-            for (int k = 0; k < KC / 16; ++k) {
-              const uint32_t ko = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
-              const uint64_t Bh = sdesc(bh + ko), Bl = sdesc(bl + ko);
-              if (ASX_DTC_ABLATE & 1) {
-              } else if (part == 0) {  // Re += Ar Wr,  Im += Ai Wr (alternating accumulators)
-                const uint32_t first = (c == 0 && k == 0) ? 0u : 1u;
-                mma_f16(d_re, sdesc(arh + ko), Bh, id, first);
-                mma_f16(d_im, sdesc(aih + ko), Bh, id, first);
-                mma_f16(d_re, sdesc(arh + ko), Bl, id, 1u);
-                mma_f16(d_im, sdesc(aih + ko), Bl, id, 1u);
-                mma_f16(d_re, sdesc(arl + ko), Bh, id, 1u);
-                mma_f16(d_im, sdesc(ail + ko), Bh, id, 1u);
-              } else {  // Re -= Ai Wi,  Im += Ar Wi
-                mma_f16(d_re, sdesc(aih + ko), Bh, idn, 1u);
-                mma_f16(d_im, sdesc(arh + ko), Bh, id, 1u);
-                mma_f16(d_re, sdesc(aih + ko), Bl, idn, 1u);
-                mma_f16(d_im, sdesc(arh + ko), Bl, id, 1u);
-                mma_f16(d_re, sdesc(ail + ko), Bh, idn, 1u);
-                mma_f16(d_im, sdesc(arl + ko), Bh, id, 1u);
+            for (int half = 0; half < 2; ++half) {
+              if (c == 0 && nt > 0) {
+                DTC_W(w0, mbar_wait(&acc_empty[half], (nt - 1) & 1));
+                tmem_fence_after();
               }
+              const uint32_t dc = (uint32_t)(half * (m / 2)), boff = (uint32_t)(half * (m / 2) * 64);
+#pragma unroll
+              for (int part = 0; part < 2; ++part) {
+                const uint32_t bh = b0 + (part ? sb1 : sb0) * B_STAGE + boff, bl = bh + (uint32_t)(b_bytes / 2);
+#pragma unroll
+                for (int k = 0; k < KC / 16; ++k) {
+                  const uint32_t ko = k * 32;  // 16 fp16 = 32 bytes along the swizzled row
+                  step(part, arh + ko, arl + ko, aih + ko, ail + ko, sdesc(bh + ko), sdesc(bl + ko), dc, idh, idhn,
+                       (c == 0 && k == 0 && part == 0) ? 0u : 1u);
+                }
+              }
+              if (c == kcn - 1) mma_commit(&acc_full[half]);
             }
-            mma_commit(&b_empty[sb]);
-            ++cb;
+            mma_commit(&b_empty[sb0]);
+            mma_commit(&b_empty[sb1]);
+            cb += 2;
+          } else {
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {  // 0: Wr, 1: Wi
+              const uint32_t sb = cb % NB;
+              DTC_W(w2, mbar_wait(&b_full[sb], (cb / NB) & 1));
+              tmem_fence_after();
+              const uint32_t bh = b0 + sb * B_STAGE, bl = bh + (uint32_t)(b_bytes / 2);
+#pragma unroll
+              for (int k = 0; k < KC / 16; ++k) {
+                const uint32_t ko = k * 32;
+                step(part, arh + ko, arl + ko, aih + ko, ail + ko, sdesc(bh + ko), sdesc(bl + ko), 0u, id, idn, 1u);
+              }
+              mma_commit(&b_empty[sb]);
+              ++cb;
+            }
           }
           mma_commit(&a_empty[sa]);
           ++ca;
         }
-        mma_commit(acc_full);
       }
+#ifdef ASX_DTC_WAITS
+      if (blockIdx.x == 0) dbg[8] = w0, dbg[9] = w1, dbg[10] = w2, dbg[12] = clock64() - t_start, dbg[13] = nt;
+#endif
     }
     __syncwarp();
   } else if (warp >= 10) {
@@ -364,7 +448,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
-      mbar_wait(&sc_empty[buf], ((it >> 1) & 1) ^ 1);
+      DTC_W(w0, mbar_wait(&sc_empty[buf], ((it >> 1) & 1) ^ 1));
       float2* sc = scale + buf * TS;
       for (int r0 = sw * (TS / (NSCALE / 32)); r0 < (sw + 1) * (TS / (NSCALE / 32)); r0 += 4) {
         float mx[4] = {0.f, 0.f, 0.f, 0.f};
@@ -405,6 +489,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
       }
       mbar_arrive(&sc_full[buf]);
     }
+#ifdef ASX_DTC_WAITS
+    if (blockIdx.x == 0 && warp == 10 && lane == 0) dbg[16] = w0, dbg[20] = clock64() - t_start, dbg[21] = it;
+#endif
   } else {
     // ------------------------------ W image loader ------------------------------
     if (lane == 0) {
@@ -413,7 +500,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
         for (int c = 0; c < kcn; ++c) {
           for (int part = 0; part < 2; ++part) {
             const uint32_t sb = cb % NB;
-            mbar_wait(&b_empty[sb], ((cb / NB) & 1) ^ 1);
+            DTC_W(w0, mbar_wait(&b_empty[sb], ((cb / NB) & 1) ^ 1));
             mbar_expect_tx(&b_full[sb], (uint32_t)b_bytes);
             const unsigned char* src = p.wimg + (size_t)(2 * c + part) * b_bytes;
             unsigned char* dst = sB + sb * B_STAGE;
@@ -423,6 +510,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
           }
         }
       }
+#ifdef ASX_DTC_WAITS
+      if (blockIdx.x == 0) dbg[24] = w0, dbg[28] = clock64() - t_start, dbg[29] = cb;
+#endif
     }
     __syncwarp();
   }
