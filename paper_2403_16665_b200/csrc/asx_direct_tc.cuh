@@ -69,7 +69,13 @@ constexpr int A_TERM = TS * KC * 2;        // one fp16 term of Ar or Ai: 8 KB
 constexpr int A_STAGE = 4 * A_TERM;        // [Ar hi | Ar lo | Ai hi | Ai lo]
 constexpr int MMAX = 256;                  // bins per tile (MMA N)
 constexpr int B_STAGE = 2 * MMAX * KC * 2; // one part (Wr or Wi) [hi | lo] at M = 256: 32 KB
-constexpr int NA = 2, NB = 3;
+#ifndef ASX_DTC_NA
+#define ASX_DTC_NA 2
+#endif
+#ifndef ASX_DTC_NB
+#define ASX_DTC_NB 3
+#endif
+constexpr int NA = ASX_DTC_NA, NB = ASX_DTC_NB;
 constexpr float W_SCALE = 256.0f;
 constexpr int SMEM_BYTES =
     1024 /*align*/ + NA * A_STAGE + NB * B_STAGE + 512 /*bars, slot*/ + 2 * 2 * TS * 4 /*scales*/;
@@ -327,14 +333,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_direct_tc(Params p) {
       const bool valid = t < ntiles;
       if (valid) {
         DTC_W(w0, mbar_wait(&sc_full[it & 1], (it >> 1) & 1));
-        // chunk 0 only: its A stage was released by the previous tile's chunk
-        // kcn - 2; chunk 1 re-uses the LAST chunk's stage and would hold the
-        // epilogue back until every MMA of the previous tile has completed
-        convert(t, it & 1, 0);
+        // NA - 1 chunks only: their A stages were released before the previous
+        // tile's last chunk; one more would re-use the LAST chunk's stage and hold
+        // the epilogue back until every MMA of the previous tile has completed
+        for (int c = 0; c < NA - 1 && c < kcn; ++c) convert(t, it & 1, c);
       }
       if (prev >= 0) DTC_W(w3, epilogue(prev, (it - 1) & 1));
       if (!valid) break;
-      for (int c = 1; c < kcn; ++c) convert(t, it & 1, c);
+      for (int c = NA - 1; c < kcn; ++c) convert(t, it & 1, c);
       prev = t;
     }
 #ifdef ASX_DTC_WAITS
