@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 ncu captures of the hot kernels (one GPU, each only after the plain run exited 0):
 #   gpurun --timeout 1500 -- bash scripts/gpu_profile.sh
-# Writes .ncu-rep files and text summaries into gpurun_out/ (copy the summaries into profiles/).
+# Writes text summaries (raw-page summary, details CSV, hottest SASS lines) into gpurun_out/; copy them into profiles/.
 set -u
 mkdir -p gpurun_out
 cap() {  # name config method kernel-regex [extra run_config args]
@@ -11,6 +11,8 @@ cap() {  # name config method kernel-regex [extra run_config args]
       python scripts/run_config.py --config $cfg --method $method --reps 2 "$@" > gpurun_out/${name}_ncu.log 2>&1
   python scripts/ncu_summary.py gpurun_out/$name.ncu-rep > gpurun_out/${name}_ncu_full_summary.txt 2>&1
   ncu -i gpurun_out/$name.ncu-rep --page details --csv > gpurun_out/${name}_ncu_details.csv 2>/dev/null
+  python scripts/ncu_hot.py gpurun_out/$name.ncu-rep 25 > gpurun_out/${name}_ncu_hot.txt 2>&1
+  rm -f gpurun_out/$name.ncu-rep  # the reports exceed gpurun's 64 MiB return limit; the text exports stay
   head -4 gpurun_out/${name}_ncu_full_summary.txt
 }
 cap r2_c4_chirp_local 4 chirp k_chirp_local
