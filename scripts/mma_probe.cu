@@ -161,6 +161,11 @@ int main() {
   run<1, 128, 256, 0>("cta_group::1 M128 N256");
   run<1, 128, 128, 0>("cta_group::1 M128 N128");
   run<1, 128, 64, 0>("cta_group::1 M128 N64");
+  run<1, 128, 32, 0>("cta_group::1 M128 N32");   // a radix-16 complex DFT pass as a real GEMM: N = 32
+  run<1, 128, 16, 0>("cta_group::1 M128 N16");
+  run<1, 64, 256, 0>("cta_group::1 M64 N256");
+  run<1, 64, 128, 0>("cta_group::1 M64 N128");
+  run<1, 64, 32, 0>("cta_group::1 M64 N32");
   run<2, 256, 256, 0>("cta_group::2 M256 N256");
   run<2, 256, 128, 0>("cta_group::2 M256 N128");
   run<1, 128, 256, 1>("cta_group::1 M128 N256 + smem stores");
