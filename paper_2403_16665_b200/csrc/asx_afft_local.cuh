@@ -16,9 +16,10 @@
 //   E2  exchange inside the half-warp (__syncwarp): -> thread (g1, g0)
 //   S3  radix-16 over n0 -> g2; only g2 < 8 (d < N/2, i.e. m < N) is kept
 //   OUT both teams park their bins in their own half-warp regions; one signal
-//       later (between the next signal's S1 and E1, after a split-phase
-//       "parked" mbarrier) all 512 threads write X[e] with e contiguous across
-//       the warp (full 32-byte sectors: the residues interleave as m = c + 2d)
+//       later (after the next signal's row reads and BEFORE its S1, behind a
+//       split-phase "parked" mbarrier) all 512 threads write X[e] with e
+//       contiguous across the warp (full 32-byte sectors: the residues
+//       interleave as m = c + 2d); the stores drain during S1
 //
 // Per residue: one team-wide and one half-warp exchange (the Stockham engine
 // needs three team-wide ones at R = 8), the α pre-twiddle folded into the
@@ -150,6 +151,18 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(cx.consumed);  // this warp is done with the staged row
   AFL_TL(2);
+  if (xcnt) {
+    // The previous signal's bins, parked by both teams at the end of the last
+    // iteration: write them now, BEFORE this signal's butterflies.  The 64 KiB
+    // of global stores drain through the SM's 32 B/clk store path in ~2 k
+    // cycles; issued here they drain while S1 keeps the FP64 pipe busy, issued
+    // after S1 (round 1) they sat in the LSU queue in front of the E1
+    // shared-memory stores (0.1517 -> 0.1409 ms, profiles/r2_c1a_experiments.md).
+    mbar_wait(cx.parked, (xcnt - 1) & 1);
+    if (live_prev) afl_copyout(p, cx.xb0, u - stride, threadIdx.x);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
+  }
   // ---- S1: × W_32^{c n2}, radix-16 over n2, × W_8192^{t (c + 2 g0)}
   if constexpr (CR == 1) {
 #pragma unroll
@@ -158,14 +171,6 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   dft_reg<16>(v);
   afl_twiddle<CR == 0 ? 1 : 0>(v, cx.tbase);
   AFL_TL(3);
-  if (xcnt) {
-    // the previous signal's bins, parked by both teams long ago: write them now,
-    // between this signal's butterflies and its first exchange
-    mbar_wait(cx.parked, (xcnt - 1) & 1);
-    if (live_prev) afl_copyout(p, cx.xb0, u - stride, threadIdx.x);
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(cx.war);
-  }
   AFL_TL(4);
   // ---- E1: (t, g0) -> thread (n0, g0); WAR: the previous signal's output reads
   if (xcnt) mbar_wait(cx.war, (xcnt - 1) & 1);
