@@ -409,6 +409,9 @@ def side_config(key, dev, stream, peak, reps=20):
     torch.cuda.synchronize()
     ms = s_.elapsed_time(e_) / reps
     kern = launched_kernel(p.method)
+    if p.fft_size > 16384:  # past one CTA: the four-step path (asx_last_launch reports its last pass only)
+        kern = ("k_large_cols + k_large_rows_local + k_large_cols (four-step chirp-z, 3 launches, csrc/asx_large.cuh)"
+                if p.method == "chirp" else "k_large_cols + k_large_rows per residue (four-step alpha-FFT, csrc/asx_large.cuh)")
     gbs = w.bytes_alg(w.batch) / (ms / 1e3) / 1e9
     res = {"workload": f"config {w.key}: batch {w.batch} x N={w.n} {w.dtype}, alpha={w.alpha}, M={w.m}",
            "method": p.method, "kernel": kern, "ms_per_step": ms, "value": w.batch * w.m / (ms / 1e3),
@@ -631,14 +634,17 @@ def run_gpu(args):
         parity["signals_checked"] = int(sum_over_ranks(parity["signals_checked"], device=dev))
         parity["pass"] = parity["max_rel_err"] <= parity["tolerance"]
 
-    # side measurements (world 1 only, not part of `value`): the other batched
-    # BASELINE configs -- 1a (the α-FFT recursion itself, the one config whose
-    # op count lets it approach the HBM roofline), 1b and 3
+    # side measurements (world 1 only, not part of `value`): the other BASELINE
+    # configs -- 1a (the α-FFT recursion itself, the one config whose op count
+    # lets it approach the HBM roofline), 1b, 3 and the two
+    # single-signal configs 0 and 2, so one line covers all five
     other = {}
     if world == 1 and not args.no_other_configs:
-        for key in ("1a", "1b", "3"):
+        for key in ("1a", "1b", "3", "0", "2"):
             if key != args.config:
                 other[key] = side_config(key, dev, stream, peak)
+                if key in ("0", "2"):  # single signals: launch latency, not throughput; config 0 sits in L2
+                    other[key]["note"] = "single signal (replicas only): device time per transform, launch-latency bound"
 
     # untimed verification collective: per-rank checksums gathered over NCCL
     checks = gather_checksums(out, device=dev)
