@@ -537,6 +537,8 @@ int asx_plan_create(asx_plan_t* out, int64_t n, int64_t a_num, int64_t a_den, in
     p->env.use_split = (no_split && no_split[0] == '1') ? 0 : 1;
     const char* no_afl = std::getenv("ASX_NO_AFFT_LOCAL");
     p->env.use_afl = (no_afl && no_afl[0] == '1') ? 0 : 1;
+    const char* no_r32 = std::getenv("ASX_NO_R32");
+    p->env.use_r32 = (no_r32 && no_r32[0] == '1') ? 0 : 1;
     const char* no_rs = std::getenv("ASX_NO_RSPLIT");
     p->env.use_rsplit = (no_rs && no_rs[0] == '1') ? 0 : 1;
     int v = 0;

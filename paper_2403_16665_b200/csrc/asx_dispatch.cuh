@@ -13,6 +13,7 @@
 #include "asx_afft_local.cuh"
 #include "asx_chirp_local.cuh"
 #include "asx_chirp_local128.cuh"
+#include "asx_chirp_r32.cuh"
 #include "asx_large.cuh"
 
 namespace asx_host {
@@ -26,6 +27,7 @@ struct LaunchEnv {
   int use_split = 1; // α-FFT residues split over two teams sharing a staged row (env ASX_NO_SPLIT=1 disables)
   int use_afl = 1;   // complex128 N = 4096, α = 1/2 α-FFT on k_afft_local (env ASX_NO_AFFT_LOCAL=1 disables)
   int use_rsplit = 1; // small α-FFT batches: one team per (signal, residue) (env ASX_NO_RSPLIT=1 disables)
+  int use_r32 = 1;   // P = 16384 complex64 chirp at 32 values per thread, k_chirp_r32 (env ASX_NO_R32=1 disables)
 };
 
 // Shape of the most recent launch on this thread (asx_last_launch, for
@@ -206,6 +208,36 @@ cudaError_t launch_persist(KParams kp, int64_t batch, cudaStream_t st, const Lau
       g_last_launch.grid = (int)grid_l;
       g_last_launch.block = CL::NT;
       g_last_launch.smem = (int)smem_l;
+      g_last_launch.staged = kp.staged;
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (KIND == KIND_CHIRP && sizeof(Real) == 4 && P == ChirpR32::P) {
+    // 32 values per thread, 4 exchanges per signal (asx_chirp_r32.cuh): one CTA per SM
+    if (env.use_r32 && env.use_local && env.use_tmem && 2 * kp.m <= P && 2 * kp.n <= P &&
+        batch < (int64_t(1) << 31)) {
+      using CR = ChirpR32;
+      auto kr = k_chirp_r32<float>;
+      size_t smem_r = CR::total(row_bytes, kp.staged != 0);
+      if (smem_r > env.smem_optin) {
+        kp.staged = 0;
+        smem_r = CR::total(row_bytes, false);
+      }
+      static thread_local int cr_attr_for = -1;
+      int dev_r = 0;
+      cudaGetDevice(&dev_r);
+      if (cr_attr_for != dev_r) {
+        cudaError_t e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env.smem_optin);
+        if (e != cudaSuccess) return e;
+        cr_attr_for = dev_r;
+      }
+      const int64_t grid_r = std::min<int64_t>(batch, env.sms);
+      kp.batch = batch;
+      kr<<<(unsigned)grid_r, CR::NT, smem_r, st>>>(kp);
+      g_last_launch.tmem = 14;
+      g_last_launch.grid = (int)grid_r;
+      g_last_launch.block = CR::NT;
+      g_last_launch.smem = (int)smem_r;
       g_last_launch.staged = kp.staged;
       return cudaGetLastError();
     }

@@ -37,15 +37,19 @@ def last_variant(asx):
 
 
 def make_plan(asx, n, a, d, m, real, legacy=False):
-    old = os.environ.get("ASX_NO_LOCAL")
+    # ASX_NO_R32=1: the 32-values-per-thread kernel (k_chirp_r32, tests/test_gpu_r32.py) takes
+    # these shapes by default; this file pins k_chirp_local, its A/B partner
+    old = {k: os.environ.get(k) for k in ("ASX_NO_LOCAL", "ASX_NO_R32")}
     os.environ["ASX_NO_LOCAL"] = "1" if legacy else "0"
+    os.environ["ASX_NO_R32"] = "1"
     try:
         return asx.plan(n, asx.DenseFactor(d, a), m=m, dtype="complex64", method="chirp", real_input=real)
     finally:
-        if old is None:
-            del os.environ["ASX_NO_LOCAL"]
-        else:
-            os.environ["ASX_NO_LOCAL"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
 
 
 CASES = [
