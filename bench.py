@@ -166,6 +166,8 @@ def launched_kernel(method: str) -> str:
     v = [ctypes.c_int() for _ in range(4)]
     _lib.lib().asx_last_launch(*[ctypes.byref(c) for c in v])
     variant = v[3].value >> 1
+    if method == "chirp" and variant == 14:
+        return "k_chirp_r32<float> (32 values per thread, 4 exchanges per signal, csrc/asx_chirp_r32.cuh)"
     if method == "chirp" and variant == 2:
         return "k_chirp_local<float> (group-local exchanges, csrc/asx_chirp_local.cuh)"
     if method == "fft" and variant == 4:

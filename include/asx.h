@@ -145,7 +145,9 @@ int asx_block_sum(const void* x, void* out, int64_t rows, int64_t len, int dtype
  * teams per CTA splitting one signal's residues, 4 the complex128 N = 4096
  * α = 1/2 group-local α-FFT k_afft_local, 6 the P = 8192 complex128
  * group-local chirp kernel k_chirp_local128, 8 the tensor-core direct form
- * k_direct_tc). */
+ * k_direct_tc, 14 the P = 16384 complex64 chirp kernel at 32 values per
+ * thread k_chirp_r32 -- the config-4 default; ASX_NO_R32=1 at plan creation
+ * falls back to k_chirp_local). */
 int asx_last_launch(int* grid, int* block, int* smem_bytes, int* staged);
 
 const char* asx_strerror(int status);

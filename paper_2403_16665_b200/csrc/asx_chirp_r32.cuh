@@ -216,9 +216,11 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
     for (int i = 0; i < 16; ++i) v[16 + i] = tw_const<32, ((ASX_R32_ACC >> 1) & 1) * ASX_R32_ACCMODE>(v[i], i);
     dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[0]));
     dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[16]));
-    tw_p1(v);
-    // ---- G1: sub-problems 2j (lo[j]) and 2j + 1 (hi[j]) -> warp j's region (WAR: the previous signal's Q3 reads)
+    // WAR on the exchange buffer (the previous signal's Q3 reads, long done by now); waited for here so
+    // that the stores below can be scheduled into the twiddle products
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
+    tw_p1(v);
+    // ---- G1: sub-problems 2j (lo[j]) and 2j + 1 (hi[j]) -> warp j's region
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       xb[j * L::REGW + t] = v[j];

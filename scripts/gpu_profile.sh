@@ -15,7 +15,7 @@ cap() {  # name config method kernel-regex [extra run_config args]
   rm -f gpurun_out/$name.ncu-rep  # the reports exceed gpurun's 64 MiB return limit; the text exports stay
   head -4 gpurun_out/${name}_ncu_full_summary.txt
 }
-cap r2_c4_chirp_local 4 chirp k_chirp_local
+cap r2_c4_chirp_r32 4 chirp k_chirp_r32
 cap r2_c1a_afft_local 1a fft k_afft_local
 cap r2_c1b_chirp_local128 1b chirp k_chirp_local128
 cap r2_c3_direct_tc 3 direct k_direct_tc

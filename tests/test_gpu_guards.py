@@ -25,8 +25,8 @@ pytestmark = pytest.mark.gpu
 
 # (label, n, alpha_b = a/d, m, dtype, method, batch) -> the kernel it launches
 KERNELS = [
-    ("k_chirp_local", 8192, 1, 8, 8192, "complex64", "chirp", 300),
-    ("k_chirp_local ragged", 6000, 1, 8, 7001, "complex64", "chirp", 151),
+    ("k_chirp_r32", 8192, 1, 8, 8192, "complex64", "chirp", 300),
+    ("k_chirp_r32 ragged", 6000, 1, 8, 7001, "complex64", "chirp", 151),
     ("k_afft_local", 4096, 1, 2, 4096, "complex128", "fft", 300),
     ("k_afft_local M < N", 4096, 1, 2, 3001, "complex128", "fft", 151),
     ("k_chirp_local128", 4096, 1, 10, 4096, "complex128", "chirp", 300),
