@@ -40,6 +40,24 @@ namespace asx {
 // latency overlaps the other's butterflies (8 columns: 128 B rows but one
 // CTA per SM, config 2 0.163 ms per column pass)
 constexpr int kColTile = ASX_COL_TILE;
+#ifndef ASX_COL_SKEW
+#define ASX_COL_SKEW 1  // column stride of the tile skewed so the kColTile columns of a row fall into distinct bank groups
+#endif
+#ifndef ASX_COL_TWCHAIN
+#define ASX_COL_TWCHAIN 1  // column-pass twiddles W^{(t + NT i) col} = W^{t col} (W^{NT col})^i: 2 table lookups per thread and tile instead of R
+#endif
+// Column stride (elements of elem_bytes) >= base: the tile is filled and drained by kColTile threads per row
+// (tau * CS + row), so tau * CS must step through the eight 16-byte bank groups (base strides are multiples of 8:
+// a 4-way conflict on every tile access, 40 % of the column passes' shared-memory wavefronts).
+constexpr int col_stride(int base, int elem_bytes) {
+#if ASX_COL_SKEW
+  const int unit = 16 / elem_bytes > 0 ? 16 / elem_bytes : 1;
+  const int mod = 8 * unit, target = unit * (8 / kColTile > 0 ? 8 / kColTile : 1);
+  return base + ((target - base % mod) + mod) % mod;
+#else
+  return base;
+#endif
+}
 template <int NT>
 constexpr int col_minb() {
   return (1024 / (NT * kColTile)) < 1 ? 1 : (1024 / (NT * kColTile)) > 16 ? 16 : (1024 / (NT * kColTile));
@@ -81,7 +99,8 @@ struct ColCfg {
   static constexpr int R = P1 < 8 ? P1 : 8;
   static constexpr int NT = P1 / R;
   using E = Fft<Real, P1, NT>;
-  static constexpr int CS = E::SMEM_ELEMS > P1 + (P1 >> E::LPAD) ? E::SMEM_ELEMS : P1 + (P1 >> E::LPAD);
+  static constexpr int CS = col_stride(E::SMEM_ELEMS > P1 + (P1 >> E::LPAD) ? E::SMEM_ELEMS : P1 + (P1 >> E::LPAD),
+                                       int(sizeof(typename CT<Real>::T)));
   static constexpr size_t SMEM = (size_t(kColTile) * CS + E::TAB_ELEMS + 2) * sizeof(typename CT<Real>::T) + 16;
 };
 
@@ -96,7 +115,7 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   const int64_t P2 = p.P2;
   // twBig period: P (chirp), r N (α-FFT; both powers of two)
   const uint64_t Pmask = MODE == COL_AFFT ? uint64_t(p.r * p.P - 1) : uint64_t(p.P - 1);
-  constexpr int CS = E::SMEM_ELEMS > P1 + (P1 >> E::LPAD) ? E::SMEM_ELEMS : P1 + (P1 >> E::LPAD);  // per-column stride
+  constexpr int CS = ColCfg<Real, P1>::CS;  // per-column stride
   extern __shared__ __align__(128) unsigned char smraw[];
   C* smbase = reinterpret_cast<C*>(smraw);
   const int team = threadIdx.x / NT, t = threadIdx.x % NT;
@@ -152,6 +171,28 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
     __syncthreads();       // tile reads done before the transform reuses sm
     E::run(v, sm, t, tr, xs);
     const int col = col0 + team;
+#if ASX_COL_TWCHAIN
+    if constexpr (MODE != COL_INV_OUT) {
+      // twiddle W^{e0 + i es}: W_P^{n2 k1}, k1 = t + NT i (chirp), W_{rN}^{(c + r d1) n2}, d1 = t + NT i (α-FFT);
+      // base and step are exact two-level lookups, the R powers at most log2 R + 1 further FP64 products
+      const C* tw = reinterpret_cast<const C*>(p.twBig);
+      const uint64_t e0 = MODE == COL_AFFT ? (uint64_t(p.c) + uint64_t(p.r) * uint64_t(t)) * uint64_t(col)
+                                           : uint64_t(t) * uint64_t(col);
+      const uint64_t es = (MODE == COL_AFFT ? uint64_t(p.r) : uint64_t(1)) * uint64_t(NT) * uint64_t(col);
+      C w[R];
+      w[0] = tw_big(tw, e0 & Pmask, p.lfBig);
+      C sp = tw_big(tw, es & Pmask, p.lfBig);
+  #pragma unroll
+      for (int step = 1; step < R; step <<= 1) {
+  #pragma unroll
+        for (int i = 0; i < step; ++i)
+          if (i + step < R) w[i + step] = cmul(w[i], sp);
+        if (2 * step < R) sp = cmul(sp, sp);
+      }
+  #pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = cmul(v[i], w[i]);
+    }
+#else
     if constexpr (MODE == COL_AFFT) {
       // twiddle W_{rN}^{(c + r d1) n2}, d1 = t + NT*i
   #pragma unroll
@@ -169,6 +210,7 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
         if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
       }
     }
+#endif
     __syncthreads();
   #pragma unroll
     for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
