@@ -539,12 +539,18 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
     // ---- Q4 = P1ᵀ -> B[k1][c], c = t + 512 i, times W_P^{k1 c}
     tw_p1(v);
     dft_reg<16>(v);
+#if ASX_COL_TWCHAIN
+    tw_chain_apply<C, 16>(v, twb, uint64_t(k1) * uint64_t(t), uint64_t(k1) * 512u, Pmask, p.lfBig);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) row[t + 512 * i] = v[i];
+#else
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const uint64_t c = uint64_t(t + 512 * i);
       row[t + 512 * i] = cmul(v[i], tw_big(twb, (uint64_t(k1) * c) & Pmask, p.lfBig));
       if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
     }
+#endif
   }
   tmem_fence_before();
   __syncthreads();

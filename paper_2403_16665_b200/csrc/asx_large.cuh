@@ -92,6 +92,32 @@ __device__ __forceinline__ C tw_big(const C* tw, uint64_t k, int lf) {
   return cmul(f, c);
 }
 
+// v[i] *= W^{e0 + i es}, i < R (W = the two-level table's root, exponents reduced by mask): base, step and
+// step^4 are exact lookups, every other power at most R / 4 + 1 further products on top of them (FP64 only: the
+// chain's rounding, a few 1e-16, is far inside the 1e-10 bound; complex64 keeps one lookup per element).
+// Replaces 2 R scattered 16-byte table loads per thread by 6 at the same number of FP64 operations.
+template <typename C, int R>
+__device__ __forceinline__ void tw_chain_apply(C (&v)[R], const C* tw, uint64_t e0, uint64_t es, uint64_t mask, int lf) {
+  const C b = tw_big(tw, e0 & mask, lf);
+  if constexpr (R < 4) {
+    v[0] = cmul(v[0], b);
+    if constexpr (R == 2) v[1] = cmul(v[1], cmul(b, tw_big(tw, es & mask, lf)));
+  } else {
+    const C s1 = tw_big(tw, es & mask, lf), s2 = cmul(s1, s1), s3 = cmul(s2, s1);
+    C wh = b;
+    C s4 = b;
+    if constexpr (R > 4) s4 = tw_big(tw, (4 * es) & mask, lf);
+#pragma unroll
+    for (int hi = 0; hi < R / 4; ++hi) {
+      v[4 * hi] = cmul(v[4 * hi], wh);
+      v[4 * hi + 1] = cmul(v[4 * hi + 1], cmul(wh, s1));
+      v[4 * hi + 2] = cmul(v[4 * hi + 2], cmul(wh, s2));
+      v[4 * hi + 3] = cmul(v[4 * hi + 3], cmul(wh, s3));
+      if (hi + 1 < R / 4) wh = cmul(wh, s4);
+    }
+  }
+}
+
 enum { COL_FWD_SIGNAL = 0, COL_FWD_TABLE = 1, COL_INV_OUT = 2, COL_AFFT = 3 };
 
 template <typename Real, int P1>
@@ -171,29 +197,14 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
     __syncthreads();       // tile reads done before the transform reuses sm
     E::run(v, sm, t, tr, xs);
     const int col = col0 + team;
-#if ASX_COL_TWCHAIN
-    if constexpr (MODE != COL_INV_OUT) {
+    if constexpr (ASX_COL_TWCHAIN && sizeof(Real) == 8 && MODE != COL_INV_OUT) {
       // twiddle W^{e0 + i es}: W_P^{n2 k1}, k1 = t + NT i (chirp), W_{rN}^{(c + r d1) n2}, d1 = t + NT i (α-FFT);
-      // base and step are exact two-level lookups, the R powers at most log2 R + 1 further FP64 products
       const C* tw = reinterpret_cast<const C*>(p.twBig);
       const uint64_t e0 = MODE == COL_AFFT ? (uint64_t(p.c) + uint64_t(p.r) * uint64_t(t)) * uint64_t(col)
                                            : uint64_t(t) * uint64_t(col);
       const uint64_t es = (MODE == COL_AFFT ? uint64_t(p.r) : uint64_t(1)) * uint64_t(NT) * uint64_t(col);
-      C w[R];
-      w[0] = tw_big(tw, e0 & Pmask, p.lfBig);
-      C sp = tw_big(tw, es & Pmask, p.lfBig);
-  #pragma unroll
-      for (int step = 1; step < R; step <<= 1) {
-  #pragma unroll
-        for (int i = 0; i < step; ++i)
-          if (i + step < R) w[i + step] = cmul(w[i], sp);
-        if (2 * step < R) sp = cmul(sp, sp);
-      }
-  #pragma unroll
-      for (int i = 0; i < R; ++i) v[i] = cmul(v[i], w[i]);
-    }
-#else
-    if constexpr (MODE == COL_AFFT) {
+      tw_chain_apply<C, R>(v, tw, e0, es, Pmask, p.lfBig);
+    } else if constexpr (MODE == COL_AFFT) {
       // twiddle W_{rN}^{(c + r d1) n2}, d1 = t + NT*i
   #pragma unroll
       for (int i = 0; i < R; ++i) {
@@ -210,7 +221,6 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
         if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
       }
     }
-#endif
     __syncthreads();
   #pragma unroll
     for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
@@ -300,12 +310,20 @@ __global__ void __launch_bounds__(NT, 1) k_large_rows(LParams p) {
           }
         }
       }
+      if constexpr (ASX_COL_TWCHAIN && sizeof(Real) == 8) {
+        // W_P^{k1 c}, c = t + NT i
+        tw_chain_apply<C, R>(v, reinterpret_cast<const C*>(p.twBig), uint64_t(k1) * uint64_t(t),
+                             uint64_t(k1) * uint64_t(NT), Pmask, p.lfBig);
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const uint64_t c = uint64_t(t + NT * i);
-        row[t + NT * i] =
-            cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(k1) * c) & Pmask, p.lfBig));
-        if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+        for (int i = 0; i < R; ++i) row[t + NT * i] = v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const uint64_t c = uint64_t(t + NT * i);
+          row[t + NT * i] =
+              cmul(v[i], tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(k1) * c) & Pmask, p.lfBig));
+          if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
+        }
       }
     }
   }
