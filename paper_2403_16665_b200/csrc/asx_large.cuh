@@ -163,32 +163,66 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
     C* const Ag = reinterpret_cast<C*>(p.A) + g * p.P;
     C* const Xg = reinterpret_cast<C*>(p.X) + g * p.Xs;
     __syncthreads();  // the previous tile's write-out reads of smbase are done
-    // ---- gather the column tile: kColTile threads per row, rows strided ----
+    // ---- gather the column tile: kColTile threads per row, rows strided.  All of a thread's loads are issued
+    // before the first use (one HBM latency per tile instead of one per row: the bounds checks otherwise keep
+    // the compiler from hoisting the loads of later rows over the shared-memory stores of earlier ones) ----
     {
-      const int tau = threadIdx.x & (kColTile - 1);
-      for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
-        const int64_t idx = int64_t(row) * P2 + col0 + tau;  // element index
-        C val = mk(Real(0), Real(0));
-        if constexpr (MODE == COL_FWD_SIGNAL) {
-          if (idx < p.n) {  // y[n] = x[n] * chirp[n], zero past N
-            const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(xg) + idx), Real(0))
-                                   : __ldg(reinterpret_cast<const C*>(xg) + idx);
-            val = cmul(xv, __ldg(reinterpret_cast<const C*>(p.chirp) + idx));
-          }
-        } else if constexpr (MODE == COL_FWD_TABLE) {
-          val = __ldg(reinterpret_cast<const C*>(p.h) + idx);
-        } else if constexpr (MODE == COL_AFFT) {
-          // x[P2 n1 + n2] × W_{rP1}^{c n1} = W_{rN}^{c n1 P2}
-          const C xv = p.real_in ? mk(__ldg(reinterpret_cast<const Real*>(xg) + idx), Real(0))
-                                 : __ldg(reinterpret_cast<const C*>(xg) + idx);
-          val = p.c ? cmul(xv, tw_big(reinterpret_cast<const C*>(p.twBig), (uint64_t(p.c) * uint64_t(row) *
-                                                                          uint64_t(P2)) & Pmask, p.lfBig))
-                    : xv;
-        } else {
-          val = __ldg(Ag + idx);  // B[k1][c], row = k1
+      constexpr int RSTEP = THREADS / kColTile, G = P1 / RSTEP;  // rows per thread
+      const int tau = threadIdx.x & (kColTile - 1), row0 = threadIdx.x / kColTile;
+      const int64_t idx0 = int64_t(row0) * P2 + col0 + tau, istep = int64_t(RSTEP) * P2;
+      C val[G];
+      if constexpr (MODE == COL_FWD_SIGNAL) {
+        // y[n] = x[n] * chirp[n], zero past N
+        const C* ch = reinterpret_cast<const C*>(p.chirp);
+        C cw[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int64_t idx = idx0 + k * istep;
+          cw[k] = idx < p.n ? __ldg(ch + idx) : mk(Real(0), Real(0));
         }
-        smbase[tau * CS + E::pad(row)] = val;
+        if (p.real_in) {
+          Real xr[G];
+#pragma unroll
+          for (int k = 0; k < G; ++k) {
+            const int64_t idx = idx0 + k * istep;
+            xr[k] = idx < p.n ? __ldg(reinterpret_cast<const Real*>(xg) + idx) : Real(0);
+          }
+#pragma unroll
+          for (int k = 0; k < G; ++k) val[k] = cmul(mk(xr[k], Real(0)), cw[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < G; ++k) {
+            const int64_t idx = idx0 + k * istep;
+            val[k] = idx < p.n ? __ldg(reinterpret_cast<const C*>(xg) + idx) : mk(Real(0), Real(0));
+          }
+#pragma unroll
+          for (int k = 0; k < G; ++k) val[k] = cmul(val[k], cw[k]);
+        }
+      } else if constexpr (MODE == COL_FWD_TABLE) {
+#pragma unroll
+        for (int k = 0; k < G; ++k) val[k] = __ldg(reinterpret_cast<const C*>(p.h) + idx0 + k * istep);
+      } else if constexpr (MODE == COL_AFFT) {
+        // x[P2 n1 + n2] × W_{rP1}^{c n1} = W_{rN}^{c n1 P2}
+        if (p.real_in) {
+#pragma unroll
+          for (int k = 0; k < G; ++k)
+            val[k] = mk(__ldg(reinterpret_cast<const Real*>(xg) + idx0 + k * istep), Real(0));
+        } else {
+#pragma unroll
+          for (int k = 0; k < G; ++k) val[k] = __ldg(reinterpret_cast<const C*>(xg) + idx0 + k * istep);
+        }
+        if (p.c) {
+#pragma unroll
+          for (int k = 0; k < G; ++k)
+            val[k] = cmul(val[k], tw_big(reinterpret_cast<const C*>(p.twBig),
+                                         (uint64_t(p.c) * uint64_t(row0 + k * RSTEP) * uint64_t(P2)) & Pmask, p.lfBig));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < G; ++k) val[k] = __ldg(Ag + idx0 + k * istep);  // B[k1][c], row = k1
       }
+#pragma unroll
+      for (int k = 0; k < G; ++k) smbase[tau * CS + E::pad(row0 + k * RSTEP)] = val[k];
     }
     __syncthreads();
     C v[R];
@@ -226,15 +260,25 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
     for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
     __syncthreads();
     {
-      const int tau = threadIdx.x & (kColTile - 1);
-      for (int row = threadIdx.x / kColTile; row < P1; row += THREADS / kColTile) {
-        const C val = smbase[tau * CS + E::pad(row)];
-        if constexpr (MODE != COL_INV_OUT) {
-          Ag[int64_t(row) * P2 + col0 + tau] = val;
-        } else {
-          const int64_t mm = int64_t(col0 + tau) + P2 * row;  // m = c + P2 d
-          if (mm < p.m)
-            Xg[mm] = cmul(cconj(val), __ldg(reinterpret_cast<const C*>(p.chirp) + mm));
+      constexpr int RSTEP = THREADS / kColTile, G = P1 / RSTEP;
+      const int tau = threadIdx.x & (kColTile - 1), row0 = threadIdx.x / kColTile;
+      if constexpr (MODE != COL_INV_OUT) {
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int row = row0 + k * RSTEP;
+          Ag[int64_t(row) * P2 + col0 + tau] = smbase[tau * CS + E::pad(row)];
+        }
+      } else {
+        // X[m] = conj(G[m]) chirp[m], m = c + P2 d < M: the chirp loads of all rows first
+        const C* ch = reinterpret_cast<const C*>(p.chirp);
+        const int64_t mm0 = int64_t(col0 + tau) + P2 * row0, mstep = P2 * RSTEP;
+        C cw[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) cw[k] = mm0 + k * mstep < p.m ? __ldg(ch + mm0 + k * mstep) : mk(Real(0), Real(0));
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const int64_t mm = mm0 + k * mstep;
+          if (mm < p.m) Xg[mm] = cmul(cconj(smbase[tau * CS + E::pad(row0 + k * RSTEP)]), cw[k]);
         }
       }
     }
