@@ -118,6 +118,14 @@ __device__ __forceinline__ void tw_chain_apply(C (&v)[R], const C* tw, uint64_t 
   }
 }
 
+#ifdef ASX_COLS_TIMELINE
+#define COLS_TL(i) do { if (threadIdx.x == 0 && blockIdx.x == 5) tl_[i] = clock64(); } while (0)
+#define COLS_TL_PRINT() do { if (threadIdx.x == 0 && blockIdx.x == 5 && un == blockIdx.x + 2 * gridDim.x) \
+  printf("cols mode %d: gather %lld sync %lld vread %lld fft %lld tw %lld sts %lld out %lld total %lld\n", MODE, tl_[1]-tl_[0], tl_[2]-tl_[1], tl_[3]-tl_[2], tl_[4]-tl_[3], tl_[5]-tl_[4], tl_[6]-tl_[5], tl_[7]-tl_[6], tl_[7]-tl_[0]); } while (0)
+#else
+#define COLS_TL(i)
+#define COLS_TL_PRINT()
+#endif
 enum { COL_FWD_SIGNAL = 0, COL_FWD_TABLE = 1, COL_INV_OUT = 2, COL_AFFT = 3 };
 
 template <typename Real, int P1>
@@ -154,6 +162,9 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
   // persistent over column tiles: the per-CTA twiddle setup (make_tw, FP64
   // sincospi seeds) is paid once per CTA instead of once per tile
   const int ntiles = int(P2 / kColTile);
+#ifdef ASX_COLS_TIMELINE
+  long long tl_[8];
+#endif
   const int64_t units = int64_t(ntiles) * p.nsig;  // (signal, column tile) pairs of the group
 #pragma unroll 1
   for (int64_t un = blockIdx.x; un < units; un += gridDim.x) {
@@ -163,6 +174,7 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
     C* const Ag = reinterpret_cast<C*>(p.A) + g * p.P;
     C* const Xg = reinterpret_cast<C*>(p.X) + g * p.Xs;
     __syncthreads();  // the previous tile's write-out reads of smbase are done
+    COLS_TL(0);
     // ---- gather the column tile: kColTile threads per row, rows strided.  All of a thread's loads are issued
     // before the first use (one HBM latency per tile instead of one per row: the bounds checks otherwise keep
     // the compiler from hoisting the loads of later rows over the shared-memory stores of earlier ones) ----
@@ -224,12 +236,16 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
 #pragma unroll
       for (int k = 0; k < G; ++k) smbase[tau * CS + E::pad(row0 + k * RSTEP)] = val[k];
     }
+    COLS_TL(1);
     __syncthreads();
+    COLS_TL(2);
     C v[R];
   #pragma unroll
     for (int i = 0; i < R; ++i) v[i] = sm[E::pad(t + NT * i)];
     __syncthreads();       // tile reads done before the transform reuses sm
+    COLS_TL(3);
     E::run(v, sm, t, tr, xs);
+    COLS_TL(4);
     const int col = col0 + team;
     if constexpr (ASX_COL_TWCHAIN && sizeof(Real) == 8 && MODE != COL_INV_OUT) {
       // twiddle W^{e0 + i es}: W_P^{n2 k1}, k1 = t + NT i (chirp), W_{rN}^{(c + r d1) n2}, d1 = t + NT i (α-FFT);
@@ -255,10 +271,12 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
         if ((i % ASX_FENCE_CHUNK) == ASX_FENCE_CHUNK - 1) reg_fence();
       }
     }
+    COLS_TL(5);
     __syncthreads();
   #pragma unroll
     for (int i = 0; i < R; ++i) sm[E::pad(t + NT * i)] = v[i];
     __syncthreads();
+    COLS_TL(6);
     {
       constexpr int RSTEP = THREADS / kColTile, G = P1 / RSTEP;
       const int tau = threadIdx.x & (kColTile - 1), row0 = threadIdx.x / kColTile;
@@ -282,6 +300,7 @@ __global__ void __launch_bounds__(NT* kColTile, col_minb<NT>()) k_large_cols(LPa
         }
       }
     }
+    COLS_TL(7); COLS_TL_PRINT();
   }
 }
 
