@@ -168,7 +168,7 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
 #pragma unroll
     for (int i = 1; i < 16; ++i) v[i] = tw_const<32>(v[i], i);
   }
-  dft_reg<16>(v);
+  ASX_DFT16_F64(v);
   afl_twiddle<CR == 0 ? 1 : 0>(v, cx.tbase);
   AFL_TL(3);
   AFL_TL(4);
@@ -196,7 +196,7 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   __syncwarp();
   AFL_TL(8);
   // ---- S2: radix-16 over n1, × W_256^{n0 g1}
-  dft_reg<16>(v);
+  ASX_DFT16_F64(v);
   afl_twiddle<1>(v, cx.tbase + 64);
   AFL_TL(9);
   // ---- E2 (half-warp): (n0, g1) -> thread (g1 = t & 15, g0)
@@ -208,7 +208,7 @@ __device__ __forceinline__ void afl_residue(const KParams& p, const AflCtx& cx, 
   __syncwarp();
   AFL_TL(10);
   // ---- S3: radix-16 over n0 -> g2; park bins d = hi + 16 n0 + 256 g2 < 2048
-  dft_reg<16>(v);
+  ASX_DFT16_F64(v);
   AFL_TL(11);
 #pragma unroll
   for (int g2 = 0; g2 < 8; ++g2) xb[L::out_pos(CR, hi, n0, g2)] = v[g2];

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
       }
     }
     // ---- P1: radix-16 DIF (upper half zero), × W_8192^{t k1}
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     tw_p1(v);
     // ---- G1: y_k1[t] -> region k1 (WAR: the previous signal's Q4 reads)
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
       for (int i = 0; i < 16; ++i) v[i] = sr[l + 16 * i];
     }
     // ---- P3: radix-16 DIF over n'' = l + 16 i'', × W_256^{l k3}
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     tw_p3(v);
     __syncwarp();
     // ---- L2 (half-warp): (l, k3) -> thread k3
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
 #pragma unroll
     for (int n = 0; n < 16; ++n) v[n] = sr[n + 17 * l];
     // ---- P4: radix-16 -> Y[f], × H[f], conj
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
 #pragma unroll
     for (int k0 = 0; k0 < 16; k0 += 4) {
       C hw[4];
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
       for (int k = 0; k < 4; ++k) v[k0 + k] = cconj(cmul(v[k0 + k], hw[k]));
     }
     // ---- inverse = conj(DFT(conj(.))): Q1 = P4ᵀ
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
 #pragma unroll
     for (int n = 0; n < 16; ++n) sr[n + 17 * l] = v[n];  // L2ᵀ: the slots this thread read
     __syncwarp();
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
     for (int k3 = 0; k3 < 16; ++k3) v[k3] = sr[l + 17 * k3];
     // ---- Q2 = P3ᵀ
     tw_p3(v);
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     if (ASX_CL128_SHFL) {
       // ---- L1ᵀ (lane-pair swap) and Q3 = P2ᵀ: (A, B) -> (A + W B, A - W B) at (n', n' + 256);
       // the shuffles order every lane's Q2 reads before the writes below
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
     ++xcnt;
     // ---- Q4 = P1ᵀ: × W_8192^{t k1}, radix-16 -> X[t + 512 i], i < 8
     tw_p1(v);
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     {
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
 #pragma unroll
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = row[t + 512 * i];
     // ---- P1: radix-16 DIF, × W_8192^{t k1'}
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     tw_p1(v);
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
 #pragma unroll
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
       }
     }
     // ---- P3, L2, P4
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     tw_p3(v);
     __syncwarp();
 #pragma unroll
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
     __syncwarp();
 #pragma unroll
     for (int n = 0; n < 16; ++n) v[n] = sr[n + 17 * l];
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     // ---- × Ht (permuted row: this thread's bins are contiguous across the CTA), conj
     {
       const C* hr = Ht + int64_t(k1) * L::P + t;
@@ -509,14 +509,14 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
       }
     }
     // ---- Q1, L2ᵀ, Q2
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
 #pragma unroll
     for (int n = 0; n < 16; ++n) sr[n + 17 * l] = v[n];
     __syncwarp();
 #pragma unroll
     for (int k3 = 0; k3 < 16; ++k3) v[k3] = sr[l + 17 * k3];
     tw_p3(v);
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
     // ---- L1ᵀ (lane-pair swap) + Q3
     {
       const C wj = w512();
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
     ++xcnt;
     // ---- Q4 = P1ᵀ -> B[k1][c], c = t + 512 i, times W_P^{k1 c}
     tw_p1(v);
-    dft_reg<16>(v);
+    ASX_DFT16_F64(v);
 #if ASX_COL_TWCHAIN
     tw_chain_apply<C, 16>(v, twb, uint64_t(k1) * uint64_t(t), uint64_t(k1) * 512u, Pmask, p.lfBig);
 #pragma unroll

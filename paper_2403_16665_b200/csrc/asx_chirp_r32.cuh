@@ -41,7 +41,19 @@
 #define ASX_R32_PLAINTW 1  // P1 / Q3 odd-power twiddles W^{2j} W as plain FP32 products (0: compensated products, +2.8 % time, 1.63e-5 instead of 1.69e-5 on config 4)
 #endif
 
+#ifndef ASX_R32_DIT
+#define ASX_R32_DIT 2  // in-register DFTs in the FMA-fused decimation-in-time form: 1 exact differences, 2 differences as 2a - sum
+#endif
+
 namespace asx {
+
+#if ASX_R32_DIT
+#define R32_DFT16(x) dft_reg_dit<16, ASX_R32_DIT == 2>(x)
+#define R32_DFT32(x) dft_reg_dit<32, ASX_R32_DIT == 2>(x)
+#else
+#define R32_DFT16(x) dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(x)
+#define R32_DFT32(x) dft_reg<32, (ASX_R32_ACC & 1) * ASX_R32_ACCMODE>(x)
+#endif
 
 #if ASX_R32_PLAINTW
 #define R32_TWMUL cmul
@@ -214,8 +226,8 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
     // ---- P1: radix-32 DIF over i with a[t + 512 i] = 0 for i >= 16: first level (a, a W_32^i), two radix-16
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[16 + i] = tw_const<32, ((ASX_R32_ACC >> 1) & 1) * ASX_R32_ACCMODE>(v[i], i);
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[0]));
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[16]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[0]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[16]));
     // WAR on the exchange buffer (the previous signal's Q3 reads, long done by now); waited for here so
     // that the stores below can be scheduled into the twiddle products
     if (xcnt) mbar_wait(war, (xcnt - 1) & 1);
@@ -239,8 +251,8 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
       v[i] = rgw[lane + 32 * i];
       v[16 + i] = rgw[512 + lane + 32 * i];
     }
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[0]));
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[16]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[0]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[16]));
     tw_p2(v);
     __syncwarp();
     // ---- L1 (warp): problem q = 16 s + k2, point lane -> lane q
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
       }
     }
     // ---- P3: radix-32 over the lane index -> Y[f]; × H[f]; conj
-    dft_reg<32, (ASX_R32_ACC & 1) * ASX_R32_ACCMODE>(v);
+    R32_DFT32(v);
 #pragma unroll
     for (int f0 = 0; f0 < 32; f0 += 4) {
       C hw[4];
@@ -266,7 +278,7 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
       for (int k = 0; k < 4; ++k) v[f0 + k] = cconj(cmul(v[f0 + k], hw[k]));
     }
     // ---- inverse = conj(DFT(conj(.))): Q1 = P3ᵀ
-    dft_reg<32, (ASX_R32_ACC & 1) * ASX_R32_ACCMODE>(v);
+    R32_DFT32(v);
     __syncwarp();
     {
       float4* row = reinterpret_cast<float4*>(rgw + L::RS * lane);  // L1ᵀ: the slots this thread read
@@ -278,8 +290,8 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
     for (int q = 0; q < 32; ++q) v[q] = rgw[L::RS * q + lane];
     // ---- Q2 = P2ᵀ
     tw_p2(v);
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[0]));
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[16]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[0]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[16]));
     __syncwarp();  // every lane has read the transpose before the sub-problems are written back
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -297,8 +309,8 @@ __global__ void __launch_bounds__(512, 1) k_chirp_r32(KParams p) {
     ++xcnt;
     // ---- Q3 = P1ᵀ: × W^{k1}, two radix-16, last level X_i = E_i + W_32^i O_i kept for i < 16
     tw_p1(v);
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[0]));
-    dft_reg<16, ((ASX_R32_ACC >> 2) & 1) * ASX_R32_ACCMODE>(reinterpret_cast<C(&)[16]>(v[16]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[0]));
+    R32_DFT16(reinterpret_cast<C(&)[16]>(v[16]));
     {
       C* X = reinterpret_cast<C*>(p.X) + int64_t(u) * p.Xs;
 #pragma unroll
