@@ -356,6 +356,9 @@ __global__ void __launch_bounds__(512, 1) k_chirp_local128(KParams p) {
 // into the row.  Persistent over rows, the next row of A and of Ht prefetched
 // into L2.  2 CTA-wide exchanges per row instead of the engine's 6.
 // ---------------------------------------------------------------------------
+#ifndef ASX_ROWS_HT_EARLY
+#define ASX_ROWS_HT_EARLY 1
+#endif
 struct RowsLocal {
   using L = ChirpLocal128;
   static constexpr size_t T3_OFF = align_up(size_t(L::XB) * sizeof(double2), 128);
@@ -495,15 +498,23 @@ __global__ void __launch_bounds__(512, 1) k_large_rows_local(LParams p) {
     __syncwarp();
 #pragma unroll
     for (int n = 0; n < 16; ++n) v[n] = sr[n + 17 * l];
-    ASX_DFT16_F64(v);
-    // ---- × Ht (permuted row: this thread's bins are contiguous across the CTA), conj
+    // ---- × Ht (permuted row: this thread's bins are contiguous across the CTA), conj; the first half of the
+    // spectrum values is requested before P4's butterflies so its L2 latency runs under them
     {
       const C* hr = Ht + int64_t(k1) * L::P + t;
+      C hw[8];
+#if ASX_ROWS_HT_EARLY
+#pragma unroll
+      for (int k = 0; k < 8; ++k) hw[k] = __ldg(hr + 512 * k);
+      reg_fence();
+#endif
+      ASX_DFT16_F64(v);
 #pragma unroll
       for (int k0 = 0; k0 < 16; k0 += 8) {
-        C hw[8];
+        if (k0 || !ASX_ROWS_HT_EARLY) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) hw[k] = __ldg(hr + 512 * (k0 + k));
+          for (int k = 0; k < 8; ++k) hw[k] = __ldg(hr + 512 * (k0 + k));
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k0 + k] = cconj(cmul(v[k0 + k], hw[k]));
       }
